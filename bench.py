@@ -1,0 +1,340 @@
+"""Benchmark of the LSGD synchronous update step (BASELINE.json metric: samples/sec at 1/2/4/8 B200).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--workload cfg3|cfg1|cfg4]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU; driver-launched for N > 1)
+
+Default workload (N=1 and the scaling run): BASELINE cfg3 — wide MLP 4096-8192-8192-512 (P = 104,874,496 fp32),
+synthetic Gaussian blobs (n = 65,536), B_loc = 512 samples per GPU (weak scaling), layout G x k with
+G = min(2, N) communicator groups (N=8 -> 2 x 4 as BASELINE cfg3 names), momentum SGD. A step = io (shard index
+H2D + row gather), postponed broadcast+update of the previous round, forward/backward, ordered intra-group
+reduce, inter-group NCCL average on the side stream.
+
+`value`  : samples/s over K steps with the dataset resident in HBM, device-timed (CUDA events on the rank's
+           stream), max over ranks.
+`e2e`    : the same metric through the C-ABI data-loader call with HOST buffers: each step's shard rows are
+           copied H2D from pinned memory and the round's loss is read back D2H inside the timed region.
+`roofline`: the dominant kernel family (the tensor-core GEMM sequence of forward+backward) against the measured
+           dense-GEMM peak in MEASURED_PEAKS.json; the reduce/update kernels are reported in `kernels`.
+`cpu_baseline`: the reference's own run_train (oracle/_ref, built from /root/reference sources) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "samples/sec (LSGD step, weak scaling, B_loc per GPU)"
+UNIT = "samples/s"
+
+
+def workload(name: str, n: int, bloc: int | None, algo: str):
+    import paper_1906_05936_b200 as lsgd
+
+    G = min(2, n) if algo == "lsgd" else 1
+    if name == "cfg3":
+        layers = [4096, 8192, 8192, 512]
+        cfg = lsgd.TrainConfig(algorithm=algo, n_workers=n, n_groups=G, layer_sizes=layers, n_samples=65536,
+                               n_features=4096, n_classes=512, spread=10.0, mode="momentum",
+                               local_batch=bloc or 512, iterations=1 << 30, seed=42)
+    elif name == "cfg1":
+        cfg = lsgd.TrainConfig(algorithm=algo, n_workers=n, n_groups=G, layer_sizes=[32, 16, 10], n_samples=5000,
+                               n_features=32, n_classes=10, spread=10.0, mode="momentum",
+                               local_batch=bloc or 16, iterations=1 << 30, seed=42)
+    elif name == "cfg4":
+        cfg = lsgd.TrainConfig(algorithm=algo, n_workers=n, n_groups=G, layer_sizes=[32, 16, 10], n_samples=5000,
+                               mode="momentum", local_batch=bloc or 64, iterations=1 << 30, seed=42)
+        cfg.b200.model = "synthetic_gradient"
+        cfg.b200.synthetic_params = 25_600_000
+    else:
+        raise SystemExit(f"unknown workload {name}")
+    cfg.b200.global_allreduce = "nccl"
+    if algo == "csgd":
+        cfg.b200.csgd_nccl = True
+    return cfg
+
+
+def flops_per_sample(layers):
+    """F = 2*sum in*out (fwd) + 2*sum in*out (dW) + 2*sum_{k>=1} in*out (dX; layer 0 skipped, mlp.cpp:116)."""
+    f = sum(2 * layers[k] * layers[k + 1] for k in range(len(layers) - 1))
+    return 2 * f + sum(2 * layers[k] * layers[k + 1] for k in range(1, len(layers) - 1))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.stop = gpu, [], threading.Event()
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def finish(self):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for i, nm in enumerate(names):
+                    if r[5 + i].lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx or None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+# ------------------------------------------------------------------------------------------------ reference arm
+def cpu_reference(cfg_name: str, n: int, steps: int, warmup: int, bloc: int | None, algo: str):
+    """The reference's own run_train (UNMODIFIED sources, oracle/_ref) timed on the host cores."""
+    from oracle import Oracle, TrainSpec
+
+    cores = os.cpu_count() or 1
+    # libgomp reads OMP_NUM_THREADS when the reference library loads; the survey found OpenMP per-sample passes
+    # slower than serial, so the rank threads supply the parallelism and OpenMP gets the remaining cores.
+    os.environ.setdefault("OMP_NUM_THREADS", str(max(1, min(cores, 8) // max(1, n))))
+    ref = Oracle("reference")
+    if cfg_name == "cfg3":
+        # OpenMP gradient scratch is min(32, B) x P doubles (mlp.cpp:243-245): keep B_loc small, dataset small
+        b = max(1, min(8, cores // max(1, n)))
+        spec = TrainSpec(algorithm=algo, n_workers=n, n_groups=min(2, n) if algo == "lsgd" else 1,
+                         layer_sizes=[4096, 8192, 8192, 512], n_samples=max(1024, 4 * b * n), n_features=4096,
+                         n_classes=512, mode="momentum", local_batch=b, iterations=steps)
+        sample = (f"run_train lsgd {spec.n_groups}x{n // spec.n_groups}, MLP 4096-8192-8192-512 fp64, B_loc={b}, "
+                  f"{steps} iterations on {spec.n_samples} blobs (per-step cost is independent of n)")
+    else:
+        b = bloc or 16
+        spec = TrainSpec(algorithm=algo, n_workers=n, n_groups=min(2, n) if algo == "lsgd" else 1,
+                         layer_sizes=[32, 16, 10], mode="momentum", local_batch=b, iterations=max(steps, 100))
+        sample = f"run_train {algo} N={n}, MLP 32-16-10 fp64, B_loc={b}, {spec.iterations} iterations"
+    if warmup:
+        w = TrainSpec(**{**spec.__dict__, "iterations": 1})
+        ref.run_train(w)
+    out = ref.run_train(spec)
+    return {"value": out["throughput_sps"], "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample,
+            "omp_threads": int(os.environ["OMP_NUM_THREADS"]), "rank_threads": spec.n_workers + spec.n_groups}
+
+
+def run_reference_arm(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return 0
+    cb = cpu_reference(args.workload, args.gpus, args.steps, args.warmup, args.bloc, args.algo)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.workload} on host cores (reference CPU implementation)",
+                       "algorithm": args.algo},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------------ b200 arm
+def run_b200_arm(args):
+    import numpy as np
+    import torch
+
+    from paper_1906_05936_b200.executors import Rank
+
+    rank, local, world = dist_env()
+    n = world if world > 1 else args.gpus
+    if world == 1 and args.gpus > 1:
+        raise SystemExit("for --gpus > 1 launch with torchrun (one process per GPU)")
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+        pg = dist
+
+    def barrier():
+        if pg:
+            pg.barrier()
+
+    def allgather(obj):
+        if not pg:
+            return [obj]
+        out = [None] * world
+        pg.all_gather_object(out, obj)
+        return out
+
+    cfg = workload(args.workload, n, args.bloc, args.algo)
+    t_setup = time.time()
+    r = Rank(cfg, rank, local)
+    r.connect(allgather(r.export()))
+    r.synchronize()
+    setup_s = time.time() - t_setup
+    stream = torch.cuda.ExternalStream(r.stream())
+
+    # warm-up, then K timed steps bracketed by barrier + sync (max over ranks)
+    r.step(args.warmup)
+    r.synchronize()
+    barrier()
+    r.timing(True)
+    clocks = ClockSampler(local) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    l0 = r.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    r.synchronize()
+    barrier()
+    ev0.record(stream)
+    r.step(args.steps)
+    ev1.record(stream)
+    r.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = r.launches() - l0
+    clk = clocks.finish() if clocks else None
+    r.timing(False)
+    fams = {f: r.kernel_time(f) for f in ("gemm", "reduce", "global", "update", "gather")}
+    ms_all = allgather(ms)
+    ms_max = max(ms_all)
+    B = cfg.local_batch
+    value = args.steps * n * B / (ms_max / 1e3)
+
+    # e2e: host rows -> H2D per step, loss D2H per step, through the C-ABI data-loader call
+    e2e = None
+    if cfg.b200.model == "mlp" and not args.skip_e2e:
+        d = cfg.n_features
+        from paper_1906_05936_b200 import host
+
+        K = args.steps
+        idx = host.minibatch_indices(cfg, 10_000, K)[:, rank * B:(rank + 1) * B]
+        xs = torch.empty((K, B, d), dtype=torch.float32, pin_memory=True)
+        ys = torch.empty((K, B), dtype=torch.int32, pin_memory=True)
+        # host-side gather of the shard rows (the data loader's job) happens before the timed region
+        xh, yh = host.generate_synthetic(cfg.seed, cfg.n_samples, d, cfg.n_classes, cfg.spread)
+        xs.copy_(torch.from_numpy(xh[idx].astype(np.float32)))
+        ys.copy_(torch.from_numpy(yh[idx].astype(np.int32)))
+        del xh, yh
+        r.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        ev0.record(stream)
+        losses = []
+        for t in range(K):
+            r.step_rows(xs[t].data_ptr(), ys[t].data_ptr(), 1)
+            losses.append(r.last_loss())  # D2H of the applied round's loss (synchronises the step)
+        ev1.record(stream)
+        r.synchronize()
+        e2e_ms = max(allgather(ev0.elapsed_time(ev1)))
+        e2e = {"value": K * n * B / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": B * d * 4 + B * 4,
+               "d2h_bytes_per_step": 8, "wall_s": time.perf_counter() - t0,
+               "loss_finite": bool(np.all(np.isfinite(losses)))}
+
+    # CPU baseline (rank 0, N=1 only): the reference itself on the host cores, bounded sample
+    cpu = None
+    if rank == 0 and n == 1 and not args.skip_cpu:
+        try:
+            cpu = cpu_reference(args.workload, 1, 3, 0, args.bloc, args.algo)
+        except Exception as e:  # reference build missing on this box
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        peaks = measured_peaks()
+        roof = None
+        if cfg.b200.model == "mlp":
+            F = flops_per_sample(cfg.layer_sizes)
+            gemm_ms, gemm_n = fams["gemm"]
+            ach = (B * F) / (gemm_ms / 1e3) / 1e12 if gemm_ms else None
+            peak = peaks.get("bf16_tflops_sustained") or 1400.0
+            roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                    "frac": (ach / peak) if ach else None, "traffic": None,
+                    "kernel": "forward+backward GEMM sequence per step (B_loc*F flops / its device time)",
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (3xTF32 ceiling = peak/6)",
+                    "flops_per_launch": B * F, "launches_timed": gemm_n}
+        else:
+            up_ms, _ = fams["update"]
+            P = cfg.n_params
+            bytes_ = 4 * P * (5 if cfg.mode == "momentum" else 3)
+            ach = bytes_ / (up_ms / 1e3) / 1e9 if up_ms else None
+            peak = peaks.get("hbm_gbs") or 6650.0
+            roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": (ach / peak) if ach else None,
+                    "traffic": None, "kernel": "K8 broadcast-pull + momentum update"}
+        kern = {f: {"avg_ms": v[0], "count": v[1]} for f, v in fams.items() if v[1]}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": args.workload, "model": "MLP " + "-".join(map(str, cfg.layer_sizes))
+                           if cfg.b200.model == "mlp" else f"synthetic gradient P={cfg.n_params}",
+                           "algorithm": args.algo, "layout": f"{cfg.n_groups}x{n // cfg.n_groups}",
+                           "local_batch": B, "global_batch": B * n, "n_params": cfg.n_params,
+                           "global_allreduce": cfg.b200.global_allreduce,
+                           "l2": "working set (w, v, grad, slices) >> 126 MB L2; no flush needed"},
+                "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,
+                "kernels": kern, "setup_s": setup_s}
+        print(json.dumps(line), flush=True)
+    r.close()
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg1", "cfg4"])
+    ap.add_argument("--algo", default="lsgd", choices=["lsgd", "csgd"])
+    ap.add_argument("--bloc", type=int, default=None)
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_b200_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

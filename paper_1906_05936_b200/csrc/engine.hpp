@@ -1,0 +1,92 @@
+// The LSGD step engine (executors.cpp:190-304 re-designed for one box of B200s).
+//
+// A Rank = one host thread + one GPU + two streams (main, comm). It hosts one or more workers (one per GPU in
+// production; several when fewer GPUs than workers are visible, which emulates the ranks on one device with
+// identical arithmetic). Every worker owns a peer-visible block
+//     [flags | payload (P+1 padded to k*S) | s[0] (S) | s[1] (S) | gbar (S)]
+// which other GPUs read over NVLink (CUDA IPC when ranks are processes, direct peer pointers when threads).
+// The communicator of group g is not a separate rank: its reduction is sliced across the group's k GPUs —
+// slot j sums elements [j*S, (j+1)*S) of all members' payloads in ascending worker order (the exact order of
+// transport.cpp:27-48), so the result is bitwise the rooted reduce while each GPU moves only 2(k-1)/k of the
+// vector over NVLink. Slice owners then average across groups (NCCL on the comm stream, or the ordered peer
+// variant), and every worker pulls the k averaged slices inside the fused update kernel.
+// Cross-GPU ordering uses monotone step counters (ld.acquire / st.release at system scope) in the peer block.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host.hpp"
+
+namespace lsgd_b200 {
+
+// Byte layout of a worker's peer-visible block; identical on every rank.
+struct PeerLayout {
+  int64_t flags = 0;     // u64 [0]=grad ready, [1]=slice sum ready, [2]=averaged slice ready
+  int64_t payload = 0;   // Ppad elements
+  int64_t s[2] = {0, 0};  // S elements each (double-buffered by step parity)
+  int64_t gbar = 0;      // S elements
+  int64_t total = 0;
+};
+enum : int { kFlagGrad = 0, kFlagSlice = 1, kFlagBcast = 2 };
+
+struct Geometry {
+  int64_t P = 0, P1 = 0, Ppad = 0, S = 0;  // params, +loss slot, padded payload, slice length
+  int esize = 4;
+  PeerLayout peer;
+  Geometry(const RunSpec& spec, int elem_size);
+};
+
+// Type-erased rank interface (the engine is instantiated for float and double).
+class Rank {
+ public:
+  virtual ~Rank() = default;
+  virtual int device() const = 0;
+  virtual const std::vector<int>& workers() const = 0;
+  virtual char* peer_block(int worker) = 0;                 // own blocks only
+  virtual void set_peer_base(int worker, char* base) = 0;   // as addressable from this rank's device
+  virtual void set_nccl(void* slice_comm, void* flat_comm) = 0;
+  virtual void upload_dataset(const double* x, const int32_t* y, int64_t n) = 0;
+  virtual void share_dataset_from(Rank* other) = 0;         // same-device or host-mapped dataset reuse
+  virtual void set_params(const double* w) = 0;             // every local worker
+  virtual void get_params(int worker, double* w) = 0;
+  virtual void issue_steps(int64_t n, const int32_t* host_global_or_shard_indices, bool shard_only) = 0;
+  virtual void issue_steps_rows(int64_t n, const void* x_host, const int32_t* y_host) = 0;
+  virtual void drain() = 0;
+  virtual void synchronize() = 0;
+  virtual int64_t steps_issued() const = 0;
+  virtual int64_t updates_applied() const = 0;
+  virtual void history(double* loss, double* lr, int64_t n) = 0;
+  virtual void param_history(double* out, int64_t rows) = 0;   // worker0 w_0..w_{rows-1}
+  virtual void phase_spans(int worker, double* out, int64_t T) = 0;
+  virtual double last_loss() = 0;
+  virtual int64_t launches() const = 0;
+  virtual void* main_stream() = 0;
+  virtual void set_timing(bool on) = 0;
+  virtual void kernel_time(const std::string& family, double* avg_ms, int64_t* count) = 0;
+  // Kernel seam (batch_gradient, mlp.hpp:54): gather `idx`, forward/backward, return grad [P] and mean loss.
+  virtual void compute_gradient(const int32_t* idx, double* grad, double* loss) = 0;
+  virtual void abort() = 0;
+  virtual void check_health() = 0;
+};
+
+// Build a rank hosting `workers` on `device`. history_rows > 0 keeps w_0..w_{rows-1} of worker 0 on the host.
+std::unique_ptr<Rank> make_rank(const RunSpec& spec, int device, std::vector<int> workers, int64_t history_rows);
+
+// In-process world (executor seam): one Rank per device, one host thread per Rank.
+struct TrainOutputs {
+  std::vector<double> final_params, loss, lr, history, worker_finals, phase_spans;
+  std::vector<int64_t> version_at_compute;
+  double total_wall_s = 0.0;
+  int64_t launches = 0;
+};
+void run_world(const RunSpec& spec, bool want_history, bool want_workers, TrainOutputs& out);
+void enable_phase_recording(Rank* r);
+void note_ipc_mapping(Rank* r, char* p);
+
+// Parallel, bit-exact blob generator (SplitMix64 is a counter: draw k of Rng(s) = mix(s + (k+1)*gamma)).
+void generate_blobs_parallel(uint64_t seed, int64_t n, int d, int c, double spread, double* x, int32_t* y);
+
+}  // namespace lsgd_b200

@@ -1,0 +1,470 @@
+// SIMT kernels of the LSGD step for sm_100a: shard gather (K1), the bit-faithful sequential-k GEMM used for the
+// fp64 parity mode and as the fp32 fallback (K2/K4/K5), the softmax-CE head (K3), the ordered peer sums
+// (K6/K7), the fused broadcast-pull + SGD/momentum update (K8) and the flag primitives that order them across
+// GPUs. Rounding: in EXACT mode every multiply and add rounds separately (no FMA contraction), reproducing the
+// reference's x86-64 build operation for operation (mlp.cpp:70-75, 110-123, 262-271; transport.cpp:27-48;
+// optimizer.cpp:30-38).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace lsgd_b200 {
+
+namespace {
+
+template <typename T>
+struct Rn;
+template <>
+struct Rn<float> {
+  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+  static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
+  static __device__ __forceinline__ float fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+};
+template <>
+struct Rn<double> {
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+  static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+  static __device__ __forceinline__ double fma(double a, double b, double c) { return __fma_rn(a, b, c); }
+};
+
+// 16-byte vector of T.
+template <typename T>
+struct alignas(16) Vec {
+  static constexpr int kN = 16 / sizeof(T);
+  T v[kN];
+};
+
+template <typename T>
+__device__ __forceinline__ Vec<T> ld16(const T* p) {
+  return *reinterpret_cast<const Vec<T>*>(p);
+}
+template <typename T>
+__device__ __forceinline__ void st16(T* p, const Vec<T>& v) {
+  *reinterpret_cast<Vec<T>*>(p) = v;
+}
+
+inline int grid_for(int64_t work, int threads, int cap = 148 * 8) {
+  int64_t g = (work + threads - 1) / threads;
+  if (g < 1) g = 1;
+  return static_cast<int>(g < cap ? g : cap);
+}
+
+// ------------------------------------------------------------------------------------------------ K1 gather
+template <typename T>
+__global__ void gather_kernel(const T* __restrict__ rows, const int32_t* __restrict__ labels,
+                              const int32_t* __restrict__ idx, int d, T* __restrict__ x, int32_t* __restrict__ y) {
+  const int s = blockIdx.x;
+  const int64_t r = idx[s];
+  if (threadIdx.x == 0) y[s] = labels[r];
+  const T* src = rows + r * d;
+  T* dst = x + static_cast<int64_t>(s) * d;
+  constexpr int V = Vec<T>::kN;
+  if (d % V == 0) {
+    for (int i = threadIdx.x; i < d / V; i += blockDim.x) st16(dst + i * V, ld16(src + i * V));
+  } else {
+    for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
+// ------------------------------------------------------------------------------------------------ K2/K4/K5
+constexpr int kBM = 64, kBN = 64, kBK = 16;
+
+template <typename T, bool EXACT, int EPI>
+__global__ void __launch_bounds__(256) gemm_simt_kernel(int M, int N, int K, const T* __restrict__ A, int64_t lda_m,
+                                                        int64_t lda_k, const T* __restrict__ B, int64_t ldb_k,
+                                                        int64_t ldb_n, T* __restrict__ C, int64_t ldc,
+                                                        const T* __restrict__ bias, int relu, T divisor,
+                                                        const T* __restrict__ mask) {
+  __shared__ T As[kBK][kBM + 1];
+  __shared__ T Bs[kBK][kBN + 1];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * kBN;
+  T acc[4][4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    int n = n0 + tx + 16 * j;
+    T init = (EPI == kEpiForward && n < N) ? bias[n] : T(0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i][j] = init;
+  }
+  const bool a_kfast = (lda_k == 1);
+  const bool b_nfast = (ldb_n == 1);
+  for (int k0 = 0; k0 < K; k0 += kBK) {
+    for (int e = threadIdx.x; e < kBM * kBK; e += 256) {
+      int kk, mm;
+      if (a_kfast) { kk = e % kBK; mm = e / kBK; } else { mm = e % kBM; kk = e / kBM; }
+      int m = m0 + mm, k = k0 + kk;
+      As[kk][mm] = (m < M && k < K) ? A[m * lda_m + k * lda_k] : T(0);
+    }
+    for (int e = threadIdx.x; e < kBN * kBK; e += 256) {
+      int kk, nn;
+      if (b_nfast) { nn = e % kBN; kk = e / kBN; } else { kk = e % kBK; nn = e / kBK; }
+      int n = n0 + nn, k = k0 + kk;
+      Bs[kk][nn] = (n < N && k < K) ? B[k * ldb_k + n * ldb_n] : T(0);
+    }
+    __syncthreads();
+    const int kmax = (K - k0) < kBK ? (K - k0) : kBK;  // never fold padding into the ordered sum
+    for (int kk = 0; kk < kmax; ++kk) {
+      T a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (EXACT) acc[i][j] = Rn<T>::add(acc[i][j], Rn<T>::mul(a[i], b[j]));
+          else acc[i][j] = Rn<T>::fma(a[i], b[j], acc[i][j]);
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int m = m0 + ty + 16 * i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int n = n0 + tx + 16 * j;
+      if (n >= N) continue;
+      T v = acc[i][j];
+      if (EPI == kEpiForward) {
+        if (relu && v < T(0)) v = T(0);
+      } else if (EPI == kEpiWeightGrad) {
+        v = Rn<T>::div(v, divisor);
+      } else {
+        if (!(mask[m * ldc + n] > T(0))) v = T(0);
+      }
+      C[m * ldc + n] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------ K3 head
+template <typename T>
+__device__ __forceinline__ T dexp(T x);
+template <>
+__device__ __forceinline__ float dexp<float>(float x) { return expf(x); }
+template <>
+__device__ __forceinline__ double dexp<double>(double x) { return exp(x); }
+template <typename T>
+__device__ __forceinline__ T dlog(T x);
+template <>
+__device__ __forceinline__ float dlog<float>(float x) { return logf(x); }
+template <>
+__device__ __forceinline__ double dlog<double>(double x) { return log(x); }
+
+template <typename T>
+__global__ void softmax_xent_kernel(const T* __restrict__ logits, const int32_t* __restrict__ labels, int b, int c,
+                                    T* __restrict__ delta, T* __restrict__ sample_loss) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= b) return;
+  const T* z = logits + static_cast<int64_t>(s) * c;
+  T* dz = delta + static_cast<int64_t>(s) * c;
+  T zmax = z[0];
+  for (int k = 1; k < c; ++k) zmax = (zmax < z[k]) ? z[k] : zmax;
+  T sum = T(0);
+  for (int k = 0; k < c; ++k) sum = Rn<T>::add(sum, dexp<T>(Rn<T>::sub(z[k], zmax)));
+  T lse = Rn<T>::add(zmax, dlog<T>(sum));
+  int lab = labels[s];
+  sample_loss[s] = Rn<T>::sub(lse, z[lab]);
+  for (int k = 0; k < c; ++k) {
+    T p = dexp<T>(Rn<T>::sub(z[k], lse));
+    dz[k] = (k == lab) ? Rn<T>::sub(p, T(1)) : p;
+  }
+}
+
+template <typename T>
+__global__ void mean_loss_kernel(const T* __restrict__ sample_loss, int b, T* __restrict__ out) {
+  T acc = T(0);
+  for (int s = 0; s < b; ++s) acc = Rn<T>::add(acc, sample_loss[s]);
+  *out = Rn<T>::div(acc, static_cast<T>(b));
+}
+
+template <typename T>
+__global__ void bias_grad_kernel(const T* __restrict__ delta, int b, int n_out, T* __restrict__ db) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_out) return;
+  T acc = T(0);
+  for (int s = 0; s < b; ++s) acc = Rn<T>::add(acc, delta[static_cast<int64_t>(s) * n_out + j]);
+  db[j] = Rn<T>::div(acc, static_cast<T>(b));
+}
+
+// ------------------------------------------------------------------------------------------------ K6/K7
+// 2 vectors per thread per trip, every source load of both issued before the first add (NVLink latency is
+// ~2 us; the loads of all peers for a vector are independent).
+template <typename T>
+__global__ void __launch_bounds__(256) ordered_sum_kernel(SrcList<T> src, int n_src, int64_t len, T* __restrict__ dst,
+                                                          bool add_zero, T divisor) {
+  constexpr int V = Vec<T>::kN;
+  const int64_t nvec = len / V;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nvec; i += 2 * stride) {
+    const int64_t i1 = i + stride;
+    const bool two = i1 < nvec;
+    Vec<T> acc0 = ld16(src.p[0] + i * V), acc1;
+    if (two) acc1 = ld16(src.p[0] + i1 * V);
+    for (int s = 1; s < n_src; ++s) {
+      Vec<T> x0 = ld16(src.p[s] + i * V), x1;
+      if (two) x1 = ld16(src.p[s] + i1 * V);
+#pragma unroll
+      for (int q = 0; q < V; ++q) acc0.v[q] = Rn<T>::add(acc0.v[q], x0.v[q]);
+      if (two) {
+#pragma unroll
+        for (int q = 0; q < V; ++q) acc1.v[q] = Rn<T>::add(acc1.v[q], x1.v[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      if (add_zero) {
+        acc0.v[q] = Rn<T>::add(acc0.v[q], T(0));
+        acc1.v[q] = Rn<T>::add(acc1.v[q], T(0));
+      }
+      if (divisor != T(0)) {
+        acc0.v[q] = Rn<T>::div(acc0.v[q], divisor);
+        acc1.v[q] = Rn<T>::div(acc1.v[q], divisor);
+      }
+    }
+    st16(dst + i * V, acc0);
+    if (two) st16(dst + i1 * V, acc1);
+  }
+  // scalar tail (len is padded to a vector multiple by the engine; kept for standalone callers)
+  for (int64_t e = nvec * V + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < len; e += stride) {
+    T a = src.p[0][e];
+    for (int s = 1; s < n_src; ++s) a = Rn<T>::add(a, src.p[s][e]);
+    if (add_zero) a = Rn<T>::add(a, T(0));
+    if (divisor != T(0)) a = Rn<T>::div(a, divisor);
+    dst[e] = a;
+  }
+}
+
+// ------------------------------------------------------------------------------------------------ K8
+template <typename T, bool EXACT>
+__device__ __forceinline__ void sgd_one(T& w, T& v, T d, const UpdateArgs<T>& a) {
+  if (a.mode == 0) {
+    w = EXACT ? Rn<T>::sub(w, Rn<T>::mul(a.lr, d)) : Rn<T>::fma(-a.lr, d, w);
+  } else {
+    if (EXACT) {
+      T g = Rn<T>::add(d, Rn<T>::mul(a.weight_decay, w));
+      v = Rn<T>::add(Rn<T>::mul(a.momentum, v), g);
+      w = Rn<T>::sub(w, Rn<T>::mul(a.lr, v));
+    } else {
+      T g = Rn<T>::fma(a.weight_decay, w, d);
+      v = Rn<T>::fma(a.momentum, v, g);
+      w = Rn<T>::fma(-a.lr, v, w);
+    }
+  }
+}
+
+template <typename T, bool EXACT>
+__global__ void __launch_bounds__(256) update_kernel(UpdateArgs<T> a) {
+  constexpr int V = Vec<T>::kN;
+  const int64_t nvec = a.n_params / V;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  bool bad = false;
+  const bool mom = a.mode != 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nvec; i += stride) {
+    const int64_t e = i * V;
+    const int64_t j = e / a.slice_len;  // slice_len is a multiple of V: a vector never straddles slices
+    Vec<T> d = ld16(a.slices.p[j] + (e - j * a.slice_len));
+    Vec<T> w = ld16(a.w + e), v;
+    if (mom) v = ld16(a.v + e);
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      T dq = a.post_div != T(0) ? Rn<T>::div(d.v[q], a.post_div) : d.v[q];
+      T vq = mom ? v.v[q] : T(0);
+      sgd_one<T, EXACT>(w.v[q], vq, dq, a);
+      if (mom) v.v[q] = vq;
+      bad |= !isfinite(w.v[q]);
+    }
+    st16(a.w + e, w);
+    if (mom) st16(a.v + e, v);
+  }
+  for (int64_t e = nvec * V + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e <= a.n_params;
+       e += stride) {
+    const int64_t j = e / a.slice_len;
+    T d = a.slices.p[j][e - j * a.slice_len];
+    if (a.post_div != T(0)) d = Rn<T>::div(d, a.post_div);
+    if (e == a.n_params) {  // the loss slot rides the same reduction (executors.cpp:59-63, 226)
+      if (a.loss_out) *a.loss_out = d;
+      continue;
+    }
+    T w = a.w[e], v = mom ? a.v[e] : T(0);
+    sgd_one<T, EXACT>(w, v, d, a);
+    a.w[e] = w;
+    if (mom) a.v[e] = v;
+    bad |= !isfinite(w);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x % 32) == 0) atomicOr(a.bad, 1u);
+}
+
+// ------------------------------------------------------------------------------------------------ flags
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void wait_flags_kernel(FlagList fl, int n, unsigned long long target, unsigned long long timeout_ns,
+                                  volatile int* timed_out) {
+  const int i = threadIdx.x;
+  if (i < n) {
+    const unsigned long long t0 = globaltimer();
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(fl.f[i]) : "memory");
+      if (v >= target) break;
+      if (*timed_out) break;  // another waiter (or the host, to abort) already gave up
+      if (globaltimer() - t0 > timeout_ns) {
+        *timed_out = 1;
+        __threadfence_system();
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void signal_flag_kernel(unsigned long long* f, unsigned long long v) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(v) : "memory");
+}
+
+__global__ void sleep_kernel(unsigned long long ns) {
+  const unsigned long long t0 = globaltimer();
+  while (globaltimer() - t0 < ns) __nanosleep(1000);
+}
+
+template <typename T>
+__global__ void from_f64_kernel(const double* __restrict__ s, int64_t n, T* __restrict__ d) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    d[i] = static_cast<T>(s[i]);
+}
+template <typename T>
+__global__ void to_f64_kernel(const T* __restrict__ s, int64_t n, double* __restrict__ d) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    d[i] = static_cast<double>(s[i]);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------------ launchers
+template <typename T>
+void launch_gather(const T* rows, const int32_t* labels, const int32_t* idx, int b, int d, T* x, int32_t* y,
+                   cudaStream_t st, LaunchCounter& lc) {
+  gather_kernel<T><<<b, 256, 0, st>>>(rows, labels, idx, d, x, y);
+  ++lc.n;
+}
+
+template <typename T>
+void launch_gemm_simt(int epi, bool exact, int M, int N, int K, const T* A, int64_t lda_m, int64_t lda_k, const T* B,
+                      int64_t ldb_k, int64_t ldb_n, T* C, int64_t ldc, const T* bias, int relu, T divisor,
+                      const T* mask, cudaStream_t st, LaunchCounter& lc) {
+  dim3 grid((N + kBN - 1) / kBN, (M + kBM - 1) / kBM);
+#define LSGD_GEMM_CASE(E, X)                                                                                    \
+  gemm_simt_kernel<T, X, E><<<grid, 256, 0, st>>>(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, bias, relu, \
+                                                  divisor, mask)
+  if (exact) {
+    if (epi == kEpiForward) LSGD_GEMM_CASE(kEpiForward, true);
+    else if (epi == kEpiWeightGrad) LSGD_GEMM_CASE(kEpiWeightGrad, true);
+    else LSGD_GEMM_CASE(kEpiInputGrad, true);
+  } else {
+    if (epi == kEpiForward) LSGD_GEMM_CASE(kEpiForward, false);
+    else if (epi == kEpiWeightGrad) LSGD_GEMM_CASE(kEpiWeightGrad, false);
+    else LSGD_GEMM_CASE(kEpiInputGrad, false);
+  }
+#undef LSGD_GEMM_CASE
+  ++lc.n;
+}
+
+template <typename T>
+void launch_softmax_xent(const T* logits, const int32_t* labels, int b, int c, T* delta, T* sample_loss,
+                         cudaStream_t st, LaunchCounter& lc) {
+  softmax_xent_kernel<T><<<(b + 127) / 128, 128, 0, st>>>(logits, labels, b, c, delta, sample_loss);
+  ++lc.n;
+}
+
+template <typename T>
+void launch_mean_loss(const T* sample_loss, int b, T* out, cudaStream_t st, LaunchCounter& lc) {
+  mean_loss_kernel<T><<<1, 1, 0, st>>>(sample_loss, b, out);
+  ++lc.n;
+}
+
+template <typename T>
+void launch_bias_grad(const T* delta, int b, int n_out, T* db, cudaStream_t st, LaunchCounter& lc) {
+  bias_grad_kernel<T><<<(n_out + 127) / 128, 128, 0, st>>>(delta, b, n_out, db);
+  ++lc.n;
+}
+
+template <typename T>
+void launch_ordered_sum(SrcList<T> src, int n_src, int64_t len, T* dst, bool add_zero, T divisor, cudaStream_t st,
+                        LaunchCounter& lc) {
+  int64_t work = (len / Vec<T>::kN + 1) / 2 + 1;
+  ordered_sum_kernel<T><<<grid_for(work, 256), 256, 0, st>>>(src, n_src, len, dst, add_zero, divisor);
+  ++lc.n;
+}
+
+template <typename T>
+void launch_update(const UpdateArgs<T>& a, bool exact, cudaStream_t st, LaunchCounter& lc) {
+  int g = grid_for(a.n_params / Vec<T>::kN + 1, 256);
+  if (exact) update_kernel<T, true><<<g, 256, 0, st>>>(a);
+  else update_kernel<T, false><<<g, 256, 0, st>>>(a);
+  ++lc.n;
+}
+
+void launch_wait_flags(FlagList flags, int n, unsigned long long target, unsigned long long timeout_ns,
+                       volatile int* timed_out, cudaStream_t st, LaunchCounter& lc) {
+  wait_flags_kernel<<<1, 32, 0, st>>>(flags, n, target, timeout_ns, timed_out);
+  ++lc.n;
+}
+
+void launch_signal_flag(unsigned long long* flag, unsigned long long value, cudaStream_t st, LaunchCounter& lc) {
+  signal_flag_kernel<<<1, 1, 0, st>>>(flag, value);
+  ++lc.n;
+}
+
+void launch_sleep(double seconds, cudaStream_t st, LaunchCounter& lc) {
+  if (seconds <= 0.0) return;
+  sleep_kernel<<<1, 1, 0, st>>>(static_cast<unsigned long long>(seconds * 1e9));
+  ++lc.n;
+}
+
+template <typename T>
+void launch_from_f64(const double* src, int64_t n, T* dst, cudaStream_t st, LaunchCounter& lc) {
+  from_f64_kernel<T><<<grid_for(n, 256), 256, 0, st>>>(src, n, dst);
+  ++lc.n;
+}
+template <typename T>
+void launch_to_f64(const T* src, int64_t n, double* dst, cudaStream_t st, LaunchCounter& lc) {
+  to_f64_kernel<T><<<grid_for(n, 256), 256, 0, st>>>(src, n, dst);
+  ++lc.n;
+}
+
+#define LSGD_INSTANTIATE(T)                                                                                        \
+  template void launch_gather<T>(const T*, const int32_t*, const int32_t*, int, int, T*, int32_t*, cudaStream_t,    \
+                                 LaunchCounter&);                                                                  \
+  template void launch_gemm_simt<T>(int, bool, int, int, int, const T*, int64_t, int64_t, const T*, int64_t,       \
+                                    int64_t, T*, int64_t, const T*, int, T, const T*, cudaStream_t, LaunchCounter&); \
+  template void launch_softmax_xent<T>(const T*, const int32_t*, int, int, T*, T*, cudaStream_t, LaunchCounter&);  \
+  template void launch_mean_loss<T>(const T*, int, T*, cudaStream_t, LaunchCounter&);                              \
+  template void launch_bias_grad<T>(const T*, int, int, T*, cudaStream_t, LaunchCounter&);                         \
+  template void launch_ordered_sum<T>(SrcList<T>, int, int64_t, T*, bool, T, cudaStream_t, LaunchCounter&);        \
+  template void launch_update<T>(const UpdateArgs<T>&, bool, cudaStream_t, LaunchCounter&);                        \
+  template void launch_from_f64<T>(const double*, int64_t, T*, cudaStream_t, LaunchCounter&);                      \
+  template void launch_to_f64<T>(const T*, int64_t, double*, cudaStream_t, LaunchCounter&);
+
+LSGD_INSTANTIATE(float)
+LSGD_INSTANTIATE(double)
+
+}  // namespace lsgd_b200

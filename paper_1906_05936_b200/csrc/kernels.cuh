@@ -1,0 +1,89 @@
+// Kernel launchers of the LSGD step (K1 gather, K2-K5 MLP, K6 ordered reduce, K7 ordered
+// global sum, K8 broadcast-pull + fused SGD/momentum update + finite check) and the cross-GPU flag primitives.
+// All launchers are asynchronous on `st` and count their launches in `launches` (the bench's gpu_launches).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace lsgd_b200 {
+
+constexpr int kMaxPeers = 16;
+
+// GEMM epilogues of the SIMT path.
+enum GemmEpi : int { kEpiForward = 0, kEpiWeightGrad = 1, kEpiInputGrad = 2 };
+
+struct LaunchCounter {
+  int64_t n = 0;
+};
+
+// --- K1: gather the shard's rows (device-resident dataset, or pinned host dataset through UVA) -------------
+template <typename T>
+void launch_gather(const T* rows, const int32_t* labels, const int32_t* idx, int b, int d, T* x_out, int32_t* y_out,
+                   cudaStream_t st, LaunchCounter& lc);
+
+// --- K2/K4/K5 SIMT GEMM with sequential-k accumulation:
+//     C[m,n] = init(n) + sum_{k=0..K-1} A(m,k) * B(k,n)   (k strictly ascending, one rounding per op when EXACT)
+// init = bias[n] (forward) or 0; epilogue: ReLU (forward hidden), / divisor (weight grad), mask (input grad).
+template <typename T>
+void launch_gemm_simt(int epi, bool exact, int M, int N, int K, const T* A, int64_t lda_m, int64_t lda_k, const T* B,
+                      int64_t ldb_k, int64_t ldb_n, T* C, int64_t ldc, const T* bias, int relu, T divisor,
+                      const T* mask, cudaStream_t st, LaunchCounter& lc);
+
+// --- K3: softmax cross-entropy head, one sequential pass per sample (mlp.cpp:79-102) -----------------------
+template <typename T>
+void launch_softmax_xent(const T* logits, const int32_t* labels, int b, int c, T* delta, T* sample_loss,
+                         cudaStream_t st, LaunchCounter& lc);
+// mean loss in batch order (mlp.cpp:262-271) -> *out
+template <typename T>
+void launch_mean_loss(const T* sample_loss, int b, T* out, cudaStream_t st, LaunchCounter& lc);
+// bias gradient: db[j] = (sum_s delta[s,j]) / b, s ascending
+template <typename T>
+void launch_bias_grad(const T* delta, int b, int n_out, T* db, cudaStream_t st, LaunchCounter& lc);
+
+// --- K6/K7: ordered sum over peer slices: dst[e] = ((src0[e] + src1[e]) + ... [+ 0.0]) [/ divisor] --------
+template <typename T>
+struct SrcList {
+  const T* p[kMaxPeers];
+};
+template <typename T>
+void launch_ordered_sum(SrcList<T> src, int n_src, int64_t len, T* dst, bool add_zero, T divisor,
+                        cudaStream_t st, LaunchCounter& lc);
+
+// --- K8: pull the averaged gradient slices and apply the postponed update (optimizer.cpp:24-42) ------------
+// delta[e] = slices[e / S][e % S] (/ post_div when post_div != 0, the CSGD per-worker division).
+template <typename T>
+struct UpdateArgs {
+  SrcList<T> slices;
+  int64_t slice_len;
+  int64_t n_params;
+  T* w;
+  T* v;
+  int mode;
+  T lr, momentum, weight_decay, post_div;
+  T* loss_out;        // receives delta[n_params] (the loss slot), may be null
+  unsigned* bad;      // OR-ed 1 when a non-finite parameter is produced
+};
+template <typename T>
+void launch_update(const UpdateArgs<T>& a, bool exact, cudaStream_t st, LaunchCounter& lc);
+
+// --- cross-GPU flags: monotone step counters in peer memory -------------------------------------------------
+struct FlagList {
+  const volatile unsigned long long* f[kMaxPeers];
+};
+// Spin (one CTA) until every flag >= target; on timeout writes 1 to *timed_out (host-mapped) and returns.
+void launch_wait_flags(FlagList flags, int n, unsigned long long target, unsigned long long timeout_ns,
+                       volatile int* timed_out, cudaStream_t st, LaunchCounter& lc);
+// System-scope release store of `value` after all prior work of the stream.
+void launch_signal_flag(unsigned long long* flag, unsigned long long value, cudaStream_t st, LaunchCounter& lc);
+// Device-side sleep for the injected io / link delays (executors.hpp:213-216).
+void launch_sleep(double seconds, cudaStream_t st, LaunchCounter& lc);
+
+// Convert a host-uploaded float64 buffer into T on device.
+template <typename T>
+void launch_from_f64(const double* src, int64_t n, T* dst, cudaStream_t st, LaunchCounter& lc);
+template <typename T>
+void launch_to_f64(const T* src, int64_t n, double* dst, cudaStream_t st, LaunchCounter& lc);
+
+}  // namespace lsgd_b200
