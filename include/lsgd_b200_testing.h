@@ -1,0 +1,24 @@
+/*
+ * lsgd_b200_testing.h — conformance hooks of liblsgd_b200.so (not part of the reference-facing surface).
+ * Used by tests/ to check the tensor-core GEMM against a float64 host product.
+ */
+#ifndef LSGD_B200_TESTING_H_
+#define LSGD_B200_TESTING_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* D = A * B^T on device 0 through the tcgen05 split-TF32 path (gemm_tc.cu). A is M x K stored K-major
+ * ([M][K], a_mn = 0) or MN-major ([K][M], a_mn = 1); B likewise N x K. epi: 0 forward (+bias[n], ReLU if relu),
+ * 1 weight gradient (/div), 2 input gradient (zero where mask[m*N+n] <= 0). out [M*N]. Shapes must be multiples
+ * of 128 (M), 256 (N) and 32 (K). */
+int lsgd_b200_test_gemm(int32_t a_mn, int32_t b_mn, int32_t epi, int32_t M, int32_t N, int32_t K, const float* A,
+                        const float* B, const float* bias, const float* mask, float div, int32_t relu, float* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSGD_B200_TESTING_H_ */

@@ -739,7 +739,7 @@ class RankImpl final : public Rank {
   }
   void tc_compute(Worker& w) {
     Timed tm(this, "gemm", main_);
-    tc_forward_backward(w.tc, L_, B_, reinterpret_cast<const float*>(w.x), w.y,
+    tc_forward_backward(w.tc, L_, B_, reinterpret_cast<const float*>(w.w), reinterpret_cast<const float*>(w.x), w.y,
                         reinterpret_cast<float*>(w.payload), reinterpret_cast<float*>(w.sample_loss), main_, lc_);
   }
   void tc_resplit_weights(Worker& w) {

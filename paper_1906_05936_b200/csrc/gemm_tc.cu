@@ -1,18 +1,690 @@
+// tcgen05 split-TF32 GEMM for sm_100a. See gemm_tc.cuh for the numerics.
+//
+// One CTA computes a 128 x 256 fp32 tile D = A * B^T (TN form: A is M x K, B is N x K) into TMEM:
+//   warp 0      TMA producer: per 32-wide K block, boxes of A_hi, A_lo, B_hi, B_lo -> one smem stage (96 KB)
+//   warp 1      TMEM allocator + single-thread MMA issuer: per 8-wide K step three tcgen05.mma.kind::tf32
+//               (hi*lo, lo*hi, hi*hi) accumulate into the same 256 TMEM columns; tcgen05.commit frees the stage
+//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> fused bias/ReLU | /B | ReLU-mask, fp32 output plus the
+//               hi/lo split the next GEMM consumes
+// Operands may be K-major ([rows][K]) or MN-major ([K][rows]); both are SWIZZLE_128B canonical UMMA layouts, so
+// dX (W read MN-major) and dW (delta and activations read MN-major) need no transposed copies.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
 #include "gemm_tc.cuh"
 
 namespace lsgd_b200 {
 
-bool tc_shapes_supported(const std::vector<int32_t>&, int) { return false; }
-void tc_alloc(TcWorkspace& ws, const Layout&, int, int) { ws.ready = true; }
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 32, STAGES = 2, THREADS = 192;
+constexpr int A_BYTES = BM * BK * 4;                        // 16 KB
+constexpr int B_BYTES = BN * BK * 4;                        // 32 KB
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;      // 96 KB
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;     // + alignment slack
+constexpr uint32_t TMEM_COLS = 256;
+
+enum : int { kFwd = 0, kWgrad = 1, kIgrad = 2, kRaw = 3 };
+
+struct EpiParams {
+  float* out;
+  int64_t ldo;
+  float* out_hi;
+  float* out_lo;
+  const float* bias;
+  const float* mask;
+  int64_t ldm;
+  int relu;
+  float div;
+  float* partial;  // split-K raw partial sums [splits][M][N]
+  int M, N;
+  uint32_t mn_lbo, mn_sbo, mn_layout;  // MN-major descriptor geometry (see op_desc)
+};
+
+// ------------------------------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(su32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  while (!mbar_try(b, parity)) {
+  }
+}
+__device__ __forceinline__ void tma_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accum) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+               : "memory");
+}
+
+// Shared-memory matrix descriptor, sm_100 version 1. layout: 2 = SWIZZLE_128B (K-major operands),
+// 1 = SWIZZLE_128B_BASE32B (the only MN-major layout tf32 operands support: 32-byte chunks of each 128 B MN row
+// XOR-swizzled over 4-row K atoms; written by TMA's SWIZZLE_128B_ATOM_32B).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint64_t layout) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;
+  d |= layout << 61;
+  return d;
+}
+
+// Instruction descriptor: D f32, A/B tf32, majors, N>>3, M>>4.
+__host__ __device__ constexpr uint32_t idesc_tf32(bool a_mn, bool b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(BM >> 4) << 24);
+}
+
+// Descriptor of operand tile `base` (R rows/cols of MN, 32 K) for the kk-th 8-wide K step.
+template <bool MN>
+__device__ __forceinline__ uint64_t op_desc(uint32_t base, int kk, const EpiParams& ep) {
+  // MN-major: 32-col MN chunks 4 KB apart (LBO), 4-row K atoms 512 B apart (SBO), +8 K rows = +1 KB per K step
+  if (MN) return sdesc(base + kk * 1024, ep.mn_lbo, ep.mn_sbo, ep.mn_layout);
+  // K-major: 128 B K rows, 8-row groups 1 KB apart (SBO), +32 B per 8-wide K step inside the swizzle atom
+  return sdesc(base + kk * 32, 16, 1024, 2);
+}
+
+// TMA of one operand tile (R along M/N) for K block starting at k.
+template <bool MN, int R>
+__device__ __forceinline__ void load_op(const CUtensorMap* map, uint64_t* bar, uint8_t* dst, int r0, int k) {
+  if (MN) {
+#pragma unroll
+    for (int c = 0; c < R / 32; ++c) tma_2d(map, bar, dst + c * 4096, r0 + 32 * c, k);
+  } else {
+    tma_2d(map, bar, dst, k, r0);
+  }
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void epi_store(const EpiParams& ep, int epi, int row, int col0, const float* v32) {
+  // 32 consecutive columns of one row
+  if (epi == kRaw) {
+    float* p = ep.partial + static_cast<int64_t>(row) * ep.N + col0;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(v32[i], v32[i + 1], v32[i + 2], v32[i + 3]);
+    return;
+  }
+  float o[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    float v = v32[i];
+    if (epi == kFwd) {
+      v = __fadd_rn(v, __ldg(ep.bias + col0 + i));
+      if (ep.relu && v < 0.f) v = 0.f;
+    } else if (epi == kWgrad) {
+      v = __fdiv_rn(v, ep.div);
+    } else {
+      if (!(__ldg(ep.mask + static_cast<int64_t>(row) * ep.ldm + col0 + i) > 0.f)) v = 0.f;
+    }
+    o[i] = v;
+  }
+  float* p = ep.out + static_cast<int64_t>(row) * ep.ldo + col0;
+#pragma unroll
+  for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]);
+  if (ep.out_hi) {
+    float* ph = ep.out_hi + static_cast<int64_t>(row) * ep.ldo + col0;
+    float* pl = ep.out_lo + static_cast<int64_t>(row) * ep.ldo + col0;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      float h0 = tf32_rna(o[i]), h1 = tf32_rna(o[i + 1]), h2 = tf32_rna(o[i + 2]), h3 = tf32_rna(o[i + 3]);
+      *reinterpret_cast<float4*>(ph + i) = make_float4(h0, h1, h2, h3);
+      *reinterpret_cast<float4*>(pl + i) = make_float4(tf32_rna(o[i] - h0), tf32_rna(o[i + 1] - h1),
+                                                       tf32_rna(o[i + 2] - h2), tf32_rna(o[i + 3] - h3));
+    }
+  }
+}
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
+                       const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo, int epi,
+                       int k_per_split, EpiParams ep) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ alignas(8) uint64_t full_bar[STAGES];
+  __shared__ alignas(8) uint64_t empty_bar[STAGES];
+  __shared__ alignas(8) uint64_t acc_bar;
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int k0 = blockIdx.z * k_per_split;
+  const int nkb = k_per_split / BK;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&acc_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta_hi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta_lo)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb_hi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb_lo)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = static_cast<uint32_t>(kb / STAGES) & 1u;
+        if (kb >= STAGES) mbar_wait(&empty_bar[s], ph ^ 1u);
+        uint8_t* st = smem + s * STAGE_BYTES;
+        mbar_expect_tx(&full_bar[s], STAGE_BYTES);
+        const int k = k0 + kb * BK;
+        load_op<A_MN, BM>(&ta_hi, &full_bar[s], st, m0, k);
+        load_op<A_MN, BM>(&ta_lo, &full_bar[s], st + A_BYTES, m0, k);
+        load_op<B_MN, BN>(&tb_hi, &full_bar[s], st + 2 * A_BYTES, n0, k);
+        load_op<B_MN, BN>(&tb_lo, &full_bar[s], st + 2 * A_BYTES + B_BYTES, n0, k);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(A_MN, B_MN);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = static_cast<uint32_t>(kb / STAGES) & 1u;
+        mbar_wait(&full_bar[s], ph);
+        tc_fence_after();
+        const uint32_t st = su32(smem + s * STAGE_BYTES);
+        const uint32_t a_hi = st, a_lo = st + A_BYTES, b_hi = st + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+          mma_tf32(tmem, op_desc<A_MN>(a_hi, kk, ep), op_desc<B_MN>(b_lo, kk, ep), idesc, acc);
+          mma_tf32(tmem, op_desc<A_MN>(a_lo, kk, ep), op_desc<B_MN>(b_hi, kk, ep), idesc, 1u);
+          mma_tf32(tmem, op_desc<A_MN>(a_hi, kk, ep), op_desc<B_MN>(b_hi, kk, ep), idesc, 1u);
+        }
+        mma_commit(&empty_bar[s]);  // stage s is free once these MMAs have read it
+      }
+      mma_commit(&acc_bar);
+    }
+  } else {
+    // epilogue warps 2..5 -> TMEM lane quadrant warp % 4
+    mbar_wait(&acc_bar, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const int row = m0 + q * 32 + lane;
+    EpiParams e = ep;
+    int mode = epi;
+    if (gridDim.z > 1) {
+      mode = kRaw;
+      e.partial = ep.partial + static_cast<int64_t>(blockIdx.z) * ep.M * ep.N;
+    }
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+          "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+            "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+            "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+      epi_store(e, mode, row, n0 + c, v);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+  }
+}
+
+// Split-K: sum the partial tiles in ascending split order, then the epilogue (deterministic, no atomics).
+__global__ void splitk_reduce_kernel(int splits, int epi, EpiParams ep) {
+  const int64_t total = static_cast<int64_t>(ep.M) * ep.N / 32;
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < total;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t e0 = g * 32;
+    const int row = static_cast<int>(e0 / ep.N), col = static_cast<int>(e0 % ep.N);
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = 0.f;
+    for (int s = 0; s < splits; ++s) {
+      const float* p = ep.partial + static_cast<int64_t>(s) * ep.M * ep.N + e0;
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        float4 q = *reinterpret_cast<const float4*>(p + i);
+        v[i] += q.x;
+        v[i + 1] += q.y;
+        v[i + 2] += q.z;
+        v[i + 3] += q.w;
+      }
+    }
+    epi_store(ep, epi, row, col, v);
+  }
+}
+
+__global__ void split_tf32_kernel(const float* __restrict__ x, int64_t n, float* __restrict__ hi,
+                                  float* __restrict__ lo) {
+  const int64_t n4 = n / 4;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 v = reinterpret_cast<const float4*>(x)[i];
+    float4 h = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+    reinterpret_cast<float4*>(hi)[i] = h;
+    reinterpret_cast<float4*>(lo)[i] =
+        make_float4(tf32_rna(v.x - h.x), tf32_rna(v.y - h.y), tf32_rna(v.z - h.z), tf32_rna(v.w - h.w));
+  }
+  for (int64_t i = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float h = tf32_rna(x[i]);
+    hi[i] = h;
+    lo[i] = tf32_rna(x[i] - h);
+  }
+}
+
+// Softmax-CE head for the tensor-core path: one thread per sample (same arithmetic as kernels.cu's head), also
+// writing the hi/lo split of delta for the backward GEMMs.
+__global__ void softmax_xent_split_kernel(const float* __restrict__ logits, const int32_t* __restrict__ labels, int b,
+                                          int c, float* __restrict__ delta, float* __restrict__ dhi,
+                                          float* __restrict__ dlo, float* __restrict__ sample_loss) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= b) return;
+  const float* z = logits + static_cast<int64_t>(s) * c;
+  float zmax = z[0];
+  for (int k = 1; k < c; ++k) zmax = (zmax < z[k]) ? z[k] : zmax;
+  float sum = 0.f;
+  for (int k = 0; k < c; ++k) sum = __fadd_rn(sum, expf(__fsub_rn(z[k], zmax)));
+  const float lse = __fadd_rn(zmax, logf(sum));
+  const int lab = labels[s];
+  sample_loss[s] = __fsub_rn(lse, z[lab]);
+  for (int k = 0; k < c; ++k) {
+    float p = expf(__fsub_rn(z[k], lse));
+    float d = (k == lab) ? __fsub_rn(p, 1.f) : p;
+    const int64_t at = static_cast<int64_t>(s) * c + k;
+    delta[at] = d;
+    float h = tf32_rna(d);
+    dhi[at] = h;
+    dlo[at] = tf32_rna(d - h);
+  }
+}
+
+// ------------------------------------------------------------------------------------------ host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    LSGD_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    check<Error>(p != nullptr && q == cudaDriverEntryPointSuccess, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<EncodeFn>(p);
+  }();
+  return fn;
+}
+
+// MN-major operand geometry: TMA swizzle SWIZZLE_128B_ATOM_32B + UMMA layout SWIZZLE_128B_BASE32B, LBO = MN chunk
+// stride, SBO = 4-row K atom stride. LSGD_TC_MN="lbo,sbo,layout,tma_swizzle" overrides it (bring-up only).
+struct MnGeometry {
+  uint32_t lbo = 4096, sbo = 512, layout = 1, tma_swizzle = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+};
+const MnGeometry& mn_geometry() {
+  static MnGeometry g = [] {
+    MnGeometry m;
+    if (const char* s = std::getenv("LSGD_TC_MN")) {
+      unsigned a, b, c, d;
+      if (std::sscanf(s, "%u,%u,%u,%u", &a, &b, &c, &d) == 4) m = MnGeometry{a, b, c, d};
+    }
+    return m;
+  }();
+  return g;
+}
+
+// Operand view: `rows` along M or N, `k` along K, stored K-major ([rows][ld]) or MN-major ([k][ld]).
+struct OpView {
+  const float* ptr;
+  int64_t rows, k, ld;
+  bool mn;
+};
+
+CUtensorMap make_map(const OpView& v, int tile_rows) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  cuuint64_t dims[2], strides[1];
+  cuuint32_t box[2], estr[2] = {1, 1};
+  if (v.mn) {
+    dims[0] = static_cast<cuuint64_t>(v.rows);
+    dims[1] = static_cast<cuuint64_t>(v.k);
+    box[0] = 32;
+    box[1] = BK;
+  } else {
+    dims[0] = static_cast<cuuint64_t>(v.k);
+    dims[1] = static_cast<cuuint64_t>(v.rows);
+    box[0] = BK;
+    box[1] = static_cast<cuuint32_t>(tile_rows);
+  }
+  strides[0] = static_cast<cuuint64_t>(v.ld) * 4;
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(v.ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           v.mn ? static_cast<CUtensorMapSwizzle>(mn_geometry().tma_swizzle) : CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  check<Error>(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (", static_cast<int>(r), ")");
+  return m;
+}
+
+struct GemmPlan {
+  CUtensorMap a_hi, a_lo, b_hi, b_lo;
+  bool a_mn = false, b_mn = false;
+  int M = 0, N = 0, K = 0, splits = 1, epi = 0;
+  EpiParams ep{};
+};
+
+template <bool A_MN, bool B_MN>
+void launch_variant(const GemmPlan& p, cudaStream_t st) {
+  // the dynamic-smem opt-in is per device: remember which devices this instantiation was configured on
+  static std::mutex mu;
+  static uint64_t configured = 0;
+  int dev = 0;
+  LSGD_CUDA(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!(configured >> dev & 1ull)) {
+      LSGD_CUDA(cudaFuncSetAttribute(gemm_tf32x3_kernel<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     SMEM_BYTES));
+      configured |= 1ull << dev;
+    }
+  }
+  dim3 grid(p.N / BN, p.M / BM, p.splits);
+  gemm_tf32x3_kernel<A_MN, B_MN><<<grid, THREADS, SMEM_BYTES, st>>>(p.a_hi, p.a_lo, p.b_hi, p.b_lo, p.epi,
+                                                                    p.K / p.splits, p.ep);
+}
+
+void run_plan(const GemmPlan& p, cudaStream_t st, LaunchCounter& lc) {
+  if (!p.a_mn && !p.b_mn) launch_variant<false, false>(p, st);
+  else if (!p.a_mn && p.b_mn) launch_variant<false, true>(p, st);
+  else if (p.a_mn && p.b_mn) launch_variant<true, true>(p, st);
+  else launch_variant<true, false>(p, st);
+  ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
+  if (p.splits > 1) {
+    int64_t work = static_cast<int64_t>(p.M) * p.N / 32;
+    int grid = static_cast<int>(std::min<int64_t>((work + 255) / 256, 148 * 8));
+    splitk_reduce_kernel<<<grid, 256, 0, st>>>(p.splits, p.epi, p.ep);
+    ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
+  }
+}
+
+int choose_splits(int M, int N, int K) {
+  int tiles = (M / BM) * (N / BN);
+  int s = 1;
+  while (tiles * s * 2 <= 160 && K % (BK * s * 2) == 0 && K / (s * 2) >= 4 * BK) s *= 2;
+  return s;
+}
+
+GemmPlan make_plan(const OpView& a_hi, const float* a_lo, const OpView& b_hi, const float* b_lo, int epi,
+                   const EpiParams& ep, float* partial, size_t partial_elems) {
+  GemmPlan p;
+  p.a_mn = a_hi.mn;
+  p.b_mn = b_hi.mn;
+  p.M = static_cast<int>(a_hi.rows);
+  p.N = static_cast<int>(b_hi.rows);
+  p.K = static_cast<int>(a_hi.k);
+  check<Error>(a_hi.k == b_hi.k, "gemm: K mismatch");
+  check<Error>(p.M % BM == 0 && p.N % BN == 0 && p.K % BK == 0, "gemm: shape ", p.M, "x", p.N, "x", p.K,
+               " is not a multiple of the 128x256x32 tile");
+  p.a_hi = make_map(a_hi, BM);
+  OpView al = a_hi;
+  al.ptr = a_lo;
+  p.a_lo = make_map(al, BM);
+  p.b_hi = make_map(b_hi, BN);
+  OpView bl = b_hi;
+  bl.ptr = b_lo;
+  p.b_lo = make_map(bl, BN);
+  p.epi = epi;
+  p.ep = ep;
+  const MnGeometry& g = mn_geometry();
+  p.ep.mn_lbo = g.lbo;
+  p.ep.mn_sbo = g.sbo;
+  p.ep.mn_layout = g.layout;
+  p.ep.M = p.M;
+  p.ep.N = p.N;
+  p.splits = choose_splits(p.M, p.N, p.K);
+  if (static_cast<size_t>(p.splits) * p.M * p.N > partial_elems) p.splits = 1;
+  p.ep.partial = partial;
+  return p;
+}
+
+}  // namespace
+
+// Per-layer plans of one worker's step (built once; the buffers they point at never move).
+struct TcLayer {
+  GemmPlan fwd, wgrad, igrad;
+  bool has_igrad = false;
+};
+
+bool tc_shapes_supported(const std::vector<int32_t>& layers, int batch) {
+  if (batch % BM != 0 || batch < BM) return false;
+  for (int32_t s : layers)
+    if (s % BN != 0) return false;
+  return layers.size() >= 2;
+}
+
+void tc_alloc(TcWorkspace& ws, const Layout& L, int batch, int n_features) {
+  auto dalloc = [&](size_t elems) {
+    void* p = nullptr;
+    LSGD_CUDA(cudaMalloc(&p, elems * sizeof(float)));
+    ws.bufs.push_back(p);
+    return static_cast<float*>(p);
+  };
+  const int B = batch;
+  ws.batch = B;
+  ws.w_hi = dalloc(static_cast<size_t>(L.n_params));
+  ws.w_lo = dalloc(static_cast<size_t>(L.n_params));
+  ws.x_hi = dalloc(static_cast<size_t>(B) * n_features);
+  ws.x_lo = dalloc(static_cast<size_t>(B) * n_features);
+  for (int k = 0; k < L.depth(); ++k) {
+    ws.act.push_back(dalloc(static_cast<size_t>(B) * L.out(k)));
+    ws.act_hi.push_back(dalloc(static_cast<size_t>(B) * L.out(k)));
+    ws.act_lo.push_back(dalloc(static_cast<size_t>(B) * L.out(k)));
+  }
+  const size_t wide = static_cast<size_t>(B) * std::max(L.widest(), n_features);
+  for (int i = 0; i < 2; ++i) {
+    ws.dlt[i] = dalloc(wide);
+    ws.dlt_hi[i] = dalloc(wide);
+    ws.dlt_lo[i] = dalloc(wide);
+  }
+  ws.partial_elems = static_cast<size_t>(16) << 20;  // 64 MB of split-K partials
+  ws.partial = dalloc(ws.partial_elems);
+  const int depth = L.depth();
+  for (int k = 0; k < depth; ++k) {
+    auto* tl = new TcLayer;
+    const int ni = L.in(k), no = L.out(k);
+    const float* in = k == 0 ? nullptr : ws.act[static_cast<size_t>(k - 1)];
+    (void)in;
+    const float* in_hi = k == 0 ? ws.x_hi : ws.act_hi[static_cast<size_t>(k - 1)];
+    const float* in_lo = k == 0 ? ws.x_lo : ws.act_lo[static_cast<size_t>(k - 1)];
+    const float* wk_hi = ws.w_hi + L.w_off[static_cast<size_t>(k)];
+    const float* wk_lo = ws.w_lo + L.w_off[static_cast<size_t>(k)];
+    const int di = (depth - 1 - k) & 1;  // delta of layer k lives in ping-pong slot di
+    // forward: act_k[B, no] = in[B, ni] . W_k[no, ni]^T + b_k
+    {
+      EpiParams ep{};
+      ep.out = ws.act[static_cast<size_t>(k)];
+      ep.ldo = no;
+      const bool last = k + 1 == depth;
+      ep.out_hi = last ? nullptr : ws.act_hi[static_cast<size_t>(k)];
+      ep.out_lo = last ? nullptr : ws.act_lo[static_cast<size_t>(k)];
+      ep.relu = last ? 0 : 1;
+      tl->fwd = make_plan(OpView{in_hi, B, ni, ni, false}, in_lo, OpView{wk_hi, no, ni, ni, false}, wk_lo, kFwd, ep,
+                          ws.partial, ws.partial_elems);
+    }
+    // weight grad: dW_k[no, ni] = delta_k^T[no, B] . in[B, ni] / B  (both operands read MN-major)
+    {
+      EpiParams ep{};
+      ep.ldo = ni;  // out pointer (payload) bound per step
+      ep.div = static_cast<float>(B);
+      tl->wgrad = make_plan(OpView{ws.dlt_hi[di], no, B, no, true}, ws.dlt_lo[di], OpView{in_hi, ni, B, ni, true},
+                            in_lo, kWgrad, ep, ws.partial, ws.partial_elems);
+    }
+    // input grad: delta_{k-1}[B, ni] = (delta_k[B, no] . W_k[no, ni]) * [act_{k-1} > 0]  (W read MN-major)
+    if (k > 0) {
+      EpiParams ep{};
+      ep.out = ws.dlt[di ^ 1];
+      ep.ldo = ni;
+      ep.out_hi = ws.dlt_hi[di ^ 1];
+      ep.out_lo = ws.dlt_lo[di ^ 1];
+      ep.mask = ws.act[static_cast<size_t>(k - 1)];
+      ep.ldm = ni;
+      tl->igrad = make_plan(OpView{ws.dlt_hi[di], B, no, no, false}, ws.dlt_lo[di], OpView{wk_hi, ni, no, ni, true},
+                            wk_lo, kIgrad, ep, ws.partial, ws.partial_elems);
+      tl->has_igrad = true;
+    }
+    ws.layers.push_back(tl);
+  }
+  ws.ready = true;
+}
+
 void tc_free(TcWorkspace& ws) {
   for (void* p : ws.bufs) cudaFree(p);
   ws.bufs.clear();
+  for (TcLayer* l : ws.layers) delete l;
+  ws.layers.clear();
   ws.ready = false;
 }
-void tc_split_weights(TcWorkspace&, const Layout&, const float*, cudaStream_t, LaunchCounter&) {}
-void tc_forward_backward(TcWorkspace&, const Layout&, int, const float*, const int32_t*, float*, float*, cudaStream_t,
-                         LaunchCounter&) {
-  throw Error("tcgen05 path not built");
+
+static void split(const float* x, int64_t n, float* hi, float* lo, cudaStream_t st, LaunchCounter& lc) {
+  int64_t work = (n / 4) + 1;
+  int grid = static_cast<int>(std::min<int64_t>((work + 255) / 256, 148 * 8));
+  split_tf32_kernel<<<grid, 256, 0, st>>>(x, n, hi, lo);
+  ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
+}
+
+void tc_split_weights(TcWorkspace& ws, const Layout& L, const float* w, cudaStream_t st, LaunchCounter& lc) {
+  // one pass over the whole parameter vector (biases split too; they are never read from the split copies)
+  split(w, L.n_params, ws.w_hi, ws.w_lo, st, lc);
+}
+
+void tc_forward_backward(TcWorkspace& ws, const Layout& L, int batch, const float* w, const float* x,
+                         const int32_t* y, float* payload, float* sample_loss, cudaStream_t st, LaunchCounter& lc) {
+  const int depth = L.depth();
+  const int B = batch;
+  split(x, static_cast<int64_t>(B) * L.in(0), ws.x_hi, ws.x_lo, st, lc);
+  for (int k = 0; k < depth; ++k) {
+    GemmPlan p = ws.layers[static_cast<size_t>(k)]->fwd;
+    p.ep.bias = w + L.b_off[static_cast<size_t>(k)];
+    run_plan(p, st, lc);
+  }
+  const int C = L.out(depth - 1);
+  const int top = 0;  // delta of layer depth-1 lives in slot (depth-1-(depth-1)) & 1 = 0
+  softmax_xent_split_kernel<<<(B + 127) / 128, 128, 0, st>>>(ws.act[static_cast<size_t>(depth - 1)], y, B, C,
+                                                             ws.dlt[top], ws.dlt_hi[top], ws.dlt_lo[top], sample_loss);
+  ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
+  launch_mean_loss<float>(sample_loss, B, payload + L.n_params, st, lc);
+  for (int k = depth - 1; k >= 0; --k) {
+    TcLayer* tl = ws.layers[static_cast<size_t>(k)];
+    const int di = (depth - 1 - k) & 1;
+    GemmPlan pw = tl->wgrad;
+    pw.ep.out = payload + L.w_off[static_cast<size_t>(k)];
+    run_plan(pw, st, lc);
+    launch_bias_grad<float>(ws.dlt[di], B, L.out(k), payload + L.b_off[static_cast<size_t>(k)], st, lc);
+    if (tl->has_igrad) run_plan(tl->igrad, st, lc);
+  }
+}
+
+void tc_test_gemm(int a_mn, int b_mn, int epi, int M, int N, int K, int splits_req, const float* A, const float* Bm,
+                  const float* bias, const float* mask, float div, int relu, float* out) {
+  (void)splits_req;
+  LSGD_CUDA(cudaSetDevice(0));
+  TcWorkspace ws;
+  auto dalloc = [&](size_t elems) {
+    void* p = nullptr;
+    LSGD_CUDA(cudaMalloc(&p, elems * sizeof(float)));
+    ws.bufs.push_back(p);
+    return static_cast<float*>(p);
+  };
+  const size_t na = static_cast<size_t>(M) * K, nb = static_cast<size_t>(N) * K, no = static_cast<size_t>(M) * N;
+  float *a = dalloc(na), *ah = dalloc(na), *al = dalloc(na), *b = dalloc(nb), *bh = dalloc(nb), *bl = dalloc(nb);
+  float *o = dalloc(no), *oh = dalloc(no), *ol = dalloc(no), *bs = dalloc(N), *mk = dalloc(no);
+  const size_t pe = static_cast<size_t>(16) << 20;
+  float* part = dalloc(pe);
+  LSGD_CUDA(cudaMemcpy(a, A, na * 4, cudaMemcpyHostToDevice));
+  LSGD_CUDA(cudaMemcpy(b, Bm, nb * 4, cudaMemcpyHostToDevice));
+  if (bias) LSGD_CUDA(cudaMemcpy(bs, bias, static_cast<size_t>(N) * 4, cudaMemcpyHostToDevice));
+  if (mask) LSGD_CUDA(cudaMemcpy(mk, mask, no * 4, cudaMemcpyHostToDevice));
+  LaunchCounter lc;
+  split(a, static_cast<int64_t>(na), ah, al, 0, lc);
+  split(b, static_cast<int64_t>(nb), bh, bl, 0, lc);
+  EpiParams ep{};
+  ep.out = o;
+  ep.ldo = N;
+  ep.out_hi = oh;
+  ep.out_lo = ol;
+  ep.bias = bs;
+  ep.mask = mk;
+  ep.ldm = N;
+  ep.relu = relu;
+  ep.div = div;
+  OpView va{ah, M, K, a_mn ? M : K, a_mn != 0}, vb{bh, N, K, b_mn ? N : K, b_mn != 0};
+  GemmPlan p = make_plan(va, al, vb, bl, epi, ep, part, pe);
+  run_plan(p, 0, lc);
+  LSGD_CUDA(cudaDeviceSynchronize());
+  LSGD_CUDA(cudaMemcpy(out, o, no * 4, cudaMemcpyDeviceToHost));
+  tc_free(ws);
 }
 
 }  // namespace lsgd_b200

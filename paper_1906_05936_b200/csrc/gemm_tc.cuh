@@ -1,4 +1,9 @@
-// Tensor-core (tcgen05, kind::tf32, split-TF32 x3) path for the dense-layer GEMMs of the fp32 step.
+// Tensor-core path of the fp32 step: the dense-layer GEMMs as tcgen05.mma kind::tf32
+// with the split-TF32 ("3xTF32") decomposition  a*b ~= a_hi*b_lo + a_lo*b_hi + a_hi*b_hi, where
+// a_hi = rna_tf32(a), a_lo = rna_tf32(a - a_hi); the dropped a_lo*b_lo term is ~2^-22 relative, so products are
+// fp32-grade (the parity contract needs fp32 accuracy: SURVEY §7 "hard parts" 1, 6). Operands are staged by TMA
+// (SWIZZLE_128B) from pre-split hi/lo copies that their producers write (the weight split after each update, the
+// forward/backward epilogues for activations and deltas); accumulators live in TMEM.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -11,16 +16,39 @@
 
 namespace lsgd_b200 {
 
+struct TcLayer;
+
 struct TcWorkspace {
   bool ready = false;
-  std::vector<void*> bufs;  // owned device allocations
+  int batch = 0;
+  std::vector<void*> bufs;     // owned device allocations
+  float* w_hi = nullptr;       // [P], same layout as w (only weight blocks are written)
+  float* w_lo = nullptr;
+  float* x_hi = nullptr;       // [B, d]
+  float* x_lo = nullptr;
+  std::vector<float*> act, act_hi, act_lo;  // [B, out_k] per layer
+  float* dlt[2] = {nullptr, nullptr};       // ping-pong deltas [B, widest]
+  float* dlt_hi[2] = {nullptr, nullptr};
+  float* dlt_lo[2] = {nullptr, nullptr};
+  float* partial = nullptr;    // split-K workspace
+  size_t partial_elems = 0;
+  std::vector<TcLayer*> layers;
 };
 
+// Every layer width a multiple of 256 and the local batch a multiple of 128 (tile 128 x 256, BK = 32).
 bool tc_shapes_supported(const std::vector<int32_t>& layers, int batch);
 void tc_alloc(TcWorkspace& ws, const Layout& L, int batch, int n_features);
 void tc_free(TcWorkspace& ws);
+// w -> (w_hi, w_lo) for every weight matrix (after each update).
 void tc_split_weights(TcWorkspace& ws, const Layout& L, const float* w, cudaStream_t st, LaunchCounter& lc);
-void tc_forward_backward(TcWorkspace& ws, const Layout& L, int batch, const float* x, const int32_t* y, float* payload,
-                         float* sample_loss, cudaStream_t st, LaunchCounter& lc);
+// Forward + backward of one shard: payload[0:P) = mean gradient, payload[P] = mean loss.
+void tc_forward_backward(TcWorkspace& ws, const Layout& L, int batch, const float* w, const float* x,
+                         const int32_t* y, float* payload, float* sample_loss, cudaStream_t st, LaunchCounter& lc);
+
+// Standalone GEMM for conformance tests: D = A * B^T with A [M x K], B [N x K] given in their storage major
+// (K-major: [rows][K]; MN-major: [K][rows]), epilogue 0 forward (bias, relu), 1 weight-grad (/div), 2 input-grad
+// (mask). Host buffers.
+void tc_test_gemm(int a_mn, int b_mn, int epi, int M, int N, int K, int splits, const float* A, const float* B,
+                  const float* bias, const float* mask, float div, int relu, float* out);
 
 }  // namespace lsgd_b200

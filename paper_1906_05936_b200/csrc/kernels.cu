@@ -365,6 +365,7 @@ void launch_gather(const T* rows, const int32_t* labels, const int32_t* idx, int
                    cudaStream_t st, LaunchCounter& lc) {
   gather_kernel<T><<<b, 256, 0, st>>>(rows, labels, idx, d, x, y);
   ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
 }
 
 template <typename T>
@@ -386,6 +387,7 @@ void launch_gemm_simt(int epi, bool exact, int M, int N, int K, const T* A, int6
   }
 #undef LSGD_GEMM_CASE
   ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
 }
 
 template <typename T>
@@ -393,18 +395,21 @@ void launch_softmax_xent(const T* logits, const int32_t* labels, int b, int c, T
                          cudaStream_t st, LaunchCounter& lc) {
   softmax_xent_kernel<T><<<(b + 127) / 128, 128, 0, st>>>(logits, labels, b, c, delta, sample_loss);
   ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
 }
 
 template <typename T>
 void launch_mean_loss(const T* sample_loss, int b, T* out, cudaStream_t st, LaunchCounter& lc) {
   mean_loss_kernel<T><<<1, 1, 0, st>>>(sample_loss, b, out);
   ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
 }
 
 template <typename T>
 void launch_bias_grad(const T* delta, int b, int n_out, T* db, cudaStream_t st, LaunchCounter& lc) {
   bias_grad_kernel<T><<<(n_out + 127) / 128, 128, 0, st>>>(delta, b, n_out, db);
   ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
 }
 
 template <typename T>
@@ -413,6 +418,7 @@ void launch_ordered_sum(SrcList<T> src, int n_src, int64_t len, T* dst, bool add
   int64_t work = (len / Vec<T>::kN + 1) / 2 + 1;
   ordered_sum_kernel<T><<<grid_for(work, 256), 256, 0, st>>>(src, n_src, len, dst, add_zero, divisor);
   ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
 }
 
 template <typename T>
@@ -421,34 +427,40 @@ void launch_update(const UpdateArgs<T>& a, bool exact, cudaStream_t st, LaunchCo
   if (exact) update_kernel<T, true><<<g, 256, 0, st>>>(a);
   else update_kernel<T, false><<<g, 256, 0, st>>>(a);
   ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
 }
 
 void launch_wait_flags(FlagList flags, int n, unsigned long long target, unsigned long long timeout_ns,
                        volatile int* timed_out, cudaStream_t st, LaunchCounter& lc) {
   wait_flags_kernel<<<1, 32, 0, st>>>(flags, n, target, timeout_ns, timed_out);
   ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
 }
 
 void launch_signal_flag(unsigned long long* flag, unsigned long long value, cudaStream_t st, LaunchCounter& lc) {
   signal_flag_kernel<<<1, 1, 0, st>>>(flag, value);
   ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
 }
 
 void launch_sleep(double seconds, cudaStream_t st, LaunchCounter& lc) {
   if (seconds <= 0.0) return;
   sleep_kernel<<<1, 1, 0, st>>>(static_cast<unsigned long long>(seconds * 1e9));
   ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
 }
 
 template <typename T>
 void launch_from_f64(const double* src, int64_t n, T* dst, cudaStream_t st, LaunchCounter& lc) {
   from_f64_kernel<T><<<grid_for(n, 256), 256, 0, st>>>(src, n, dst);
   ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
 }
 template <typename T>
 void launch_to_f64(const T* src, int64_t n, double* dst, cudaStream_t st, LaunchCounter& lc) {
   to_f64_kernel<T><<<grid_for(n, 256), 256, 0, st>>>(src, n, dst);
   ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
 }
 
 #define LSGD_INSTANTIATE(T)                                                                                        \

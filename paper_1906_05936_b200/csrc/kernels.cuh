@@ -7,6 +7,8 @@
 
 #include <cstdint>
 
+#include "common.hpp"
+
 namespace lsgd_b200 {
 
 constexpr int kMaxPeers = 16;

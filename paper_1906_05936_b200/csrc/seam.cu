@@ -138,3 +138,12 @@ int lsgd_b200_sgd_update(int32_t dtype, int64_t n, double* w, const double* delt
 }
 
 }  // extern "C"
+
+#include "../../include/lsgd_b200_testing.h"
+#include "gemm_tc.cuh"
+
+extern "C" int lsgd_b200_test_gemm(int32_t a_mn, int32_t b_mn, int32_t epi, int32_t M, int32_t N, int32_t K,
+                                   const float* A, const float* B, const float* bias, const float* mask, float div,
+                                   int32_t relu, float* out) {
+  return seam_guard([&] { tc_test_gemm(a_mn, b_mn, epi, M, N, K, 1, A, B, bias, mask, div, relu, out); });
+}
