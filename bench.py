@@ -281,7 +281,9 @@ def run_b200_arm(args):
         roof = None
         if cfg.b200.model == "mlp":
             F = flops_per_sample(cfg.layer_sizes)
-            gemm_ms, gemm_n = fams["gemm"]
+            avg, cnt = fams["gemm"]
+            gemm_n = cnt
+            gemm_ms = avg * cnt / args.steps  # per-layer brackets summed to one step's GEMM time
             ach = (B * F) / (gemm_ms / 1e3) / 1e12 if gemm_ms else None
             peak = peaks.get("bf16_tflops_sustained") or 1400.0
             roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
@@ -290,14 +292,16 @@ def run_b200_arm(args):
                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (3xTF32 ceiling = peak/6)",
                     "flops_per_launch": B * F, "launches_timed": gemm_n}
         else:
-            up_ms, _ = fams["update"]
+            avg, cnt = fams["update"]
+            up_ms = avg * cnt / args.steps
             P = cfg.n_params
             bytes_ = 4 * P * (5 if cfg.mode == "momentum" else 3)
             ach = bytes_ / (up_ms / 1e3) / 1e9 if up_ms else None
             peak = peaks.get("hbm_gbs") or 6650.0
             roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": (ach / peak) if ach else None,
                     "traffic": None, "kernel": "K8 broadcast-pull + momentum update"}
-        kern = {f: {"avg_ms": v[0], "count": v[1]} for f, v in fams.items() if v[1]}
+        kern = {f: {"avg_ms": v[0], "count": v[1], "ms_per_step": v[0] * v[1] / args.steps}
+                for f, v in fams.items() if v[1]}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",

@@ -24,17 +24,32 @@ namespace lsgd_b200 {
 
 // Byte layout of a worker's peer-visible block; identical on every rank.
 struct PeerLayout {
-  int64_t flags = 0;     // u64 [0]=grad ready, [1]=slice sum ready, [2]=averaged slice ready
+  int64_t flags = 0;     // u64 [which * kMaxBuckets + bucket]: which 0 = grad ready, 1 = slice sum, 2 = averaged
   int64_t payload = 0;   // Ppad elements
-  int64_t s[2] = {0, 0};  // S elements each (double-buffered by step parity)
-  int64_t gbar = 0;      // S elements
+  int64_t s[2] = {0, 0};  // Sg elements each (double-buffered by step parity)
+  int64_t gbar = 0;      // Sg elements
   int64_t total = 0;
 };
 enum : int { kFlagGrad = 0, kFlagSlice = 1, kFlagBcast = 2 };
+constexpr int kMaxBuckets = 32;
+
+// Gradient buckets: one per layer (that layer's [W_k | b_k] block, contiguous in the reference's parameter
+// layout, mlp.hpp:14-18), the loss slot riding the last layer's bucket. Each bucket is split into k sub-slices of
+// S elements; sub-slice j lives in the payload at poff + j*S and in slot j's s/gbar regions at goff.
+struct Bucket {
+  int64_t pstart = 0;  // first parameter index
+  int64_t n = 0;       // parameters (the loss slot, when carried, is bucket-local index n)
+  bool loss = false;
+  int64_t S = 0;       // sub-slice length, multiple of 64 elements
+  int64_t poff = 0;    // payload offset (elements, 64-aligned)
+  int64_t goff = 0;    // offset inside each slot's s/gbar region (64-aligned)
+};
 
 struct Geometry {
-  int64_t P = 0, P1 = 0, Ppad = 0, S = 0;  // params, +loss slot, padded payload, slice length
+  int64_t P = 0, Ppad = 0, Sg = 0;  // params, padded payload, per-slot slice elements (sum of bucket S)
   int esize = 4;
+  std::vector<Bucket> buckets;
+  int64_t loss_at = 0;             // payload index of the loss slot
   PeerLayout peer;
   Geometry(const RunSpec& spec, int elem_size);
 };

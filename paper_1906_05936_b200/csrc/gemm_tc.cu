@@ -618,32 +618,36 @@ void tc_split_weights(TcWorkspace& ws, const Layout& L, const float* w, cudaStre
   split(w, L.n_params, ws.w_hi, ws.w_lo, st, lc);
 }
 
-void tc_forward_backward(TcWorkspace& ws, const Layout& L, int batch, const float* w, const float* x,
-                         const int32_t* y, float* payload, float* sample_loss, cudaStream_t st, LaunchCounter& lc) {
+void tc_forward_layer(TcWorkspace& ws, const Layout& L, int k, const float* w, const float* x, cudaStream_t st,
+                      LaunchCounter& lc) {
+  if (k == 0) split(x, static_cast<int64_t>(ws.batch) * L.in(0), ws.x_hi, ws.x_lo, st, lc);
+  GemmPlan p = ws.layers[static_cast<size_t>(k)]->fwd;
+  p.ep.bias = w + L.b_off[static_cast<size_t>(k)];
+  run_plan(p, st, lc);
+}
+
+void tc_head(TcWorkspace& ws, const Layout& L, const int32_t* y, float* sample_loss, float* loss_out, cudaStream_t st,
+             LaunchCounter& lc) {
   const int depth = L.depth();
-  const int B = batch;
-  split(x, static_cast<int64_t>(B) * L.in(0), ws.x_hi, ws.x_lo, st, lc);
-  for (int k = 0; k < depth; ++k) {
-    GemmPlan p = ws.layers[static_cast<size_t>(k)]->fwd;
-    p.ep.bias = w + L.b_off[static_cast<size_t>(k)];
-    run_plan(p, st, lc);
-  }
+  const int B = ws.batch;
   const int C = L.out(depth - 1);
-  const int top = 0;  // delta of layer depth-1 lives in slot (depth-1-(depth-1)) & 1 = 0
+  const int top = 0;  // delta of layer depth-1 lives in ping-pong slot (depth-1-(depth-1)) & 1 = 0
   softmax_xent_split_kernel<<<(B + 127) / 128, 128, 0, st>>>(ws.act[static_cast<size_t>(depth - 1)], y, B, C,
                                                              ws.dlt[top], ws.dlt_hi[top], ws.dlt_lo[top], sample_loss);
   ++lc.n;
   LSGD_CUDA(cudaGetLastError());
-  launch_mean_loss<float>(sample_loss, B, payload + L.n_params, st, lc);
-  for (int k = depth - 1; k >= 0; --k) {
-    TcLayer* tl = ws.layers[static_cast<size_t>(k)];
-    const int di = (depth - 1 - k) & 1;
-    GemmPlan pw = tl->wgrad;
-    pw.ep.out = payload + L.w_off[static_cast<size_t>(k)];
-    run_plan(pw, st, lc);
-    launch_bias_grad<float>(ws.dlt[di], B, L.out(k), payload + L.b_off[static_cast<size_t>(k)], st, lc);
-    if (tl->has_igrad) run_plan(tl->igrad, st, lc);
-  }
+  launch_mean_loss<float>(sample_loss, B, loss_out, st, lc);
+}
+
+void tc_backward_layer(TcWorkspace& ws, const Layout& L, int k, float* gW, float* gb, cudaStream_t st,
+                       LaunchCounter& lc) {
+  TcLayer* tl = ws.layers[static_cast<size_t>(k)];
+  const int di = (L.depth() - 1 - k) & 1;
+  GemmPlan pw = tl->wgrad;
+  pw.ep.out = gW;
+  run_plan(pw, st, lc);
+  launch_bias_grad<float>(ws.dlt[di], ws.batch, L.out(k), gb, st, lc);
+  if (tl->has_igrad) run_plan(tl->igrad, st, lc);
 }
 
 void tc_test_gemm(int a_mn, int b_mn, int epi, int M, int N, int K, int splits_req, const float* A, const float* Bm,

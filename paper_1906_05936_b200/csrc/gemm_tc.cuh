@@ -39,11 +39,17 @@ struct TcWorkspace {
 bool tc_shapes_supported(const std::vector<int32_t>& layers, int batch);
 void tc_alloc(TcWorkspace& ws, const Layout& L, int batch, int n_features);
 void tc_free(TcWorkspace& ws);
-// w -> (w_hi, w_lo) for every weight matrix (after each update).
+// w -> (w_hi, w_lo) for the whole parameter vector (initial parameters; afterwards the fused update writes it).
 void tc_split_weights(TcWorkspace& ws, const Layout& L, const float* w, cudaStream_t st, LaunchCounter& lc);
-// Forward + backward of one shard: payload[0:P) = mean gradient, payload[P] = mean loss.
-void tc_forward_backward(TcWorkspace& ws, const Layout& L, int batch, const float* w, const float* x,
-                         const int32_t* y, float* payload, float* sample_loss, cudaStream_t st, LaunchCounter& lc);
+// Forward layer k (k = 0 first splits the gathered batch x): act_k = ReLU?(in . W_k^T + b_k) and its split.
+void tc_forward_layer(TcWorkspace& ws, const Layout& L, int k, const float* w, const float* x, cudaStream_t st,
+                      LaunchCounter& lc);
+// Softmax-CE head: delta of the top layer (+ split), per-sample losses, mean loss -> *loss_out.
+void tc_head(TcWorkspace& ws, const Layout& L, const int32_t* y, float* sample_loss, float* loss_out, cudaStream_t st,
+             LaunchCounter& lc);
+// Backward layer k: dW_k -> gW ([out x in], /B), db_k -> gb, and (k > 0) the masked delta of layer k-1.
+void tc_backward_layer(TcWorkspace& ws, const Layout& L, int k, float* gW, float* gb, cudaStream_t st,
+                       LaunchCounter& lc);
 
 // Standalone GEMM for conformance tests: D = A * B^T with A [M x K], B [N x K] given in their storage major
 // (K-major: [rows][K]; MN-major: [K][rows]), epilogue 0 forward (bias, relu), 1 weight-grad (/div), 2 input-grad

@@ -203,9 +203,9 @@ __global__ void bias_grad_kernel(const T* __restrict__ delta, int b, int n_out, 
 // ~2 us; the loads of all peers for a vector are independent).
 template <typename T>
 __global__ void __launch_bounds__(256) ordered_sum_kernel(SrcList<T> src, int n_src, int64_t len, T* __restrict__ dst,
-                                                          bool add_zero, T divisor) {
+                                                          bool add_zero, T divisor, bool scalar_only) {
   constexpr int V = Vec<T>::kN;
-  const int64_t nvec = len / V;
+  const int64_t nvec = scalar_only ? 0 : len / V;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nvec; i += 2 * stride) {
     const int64_t i1 = i + stride;
@@ -264,10 +264,41 @@ __device__ __forceinline__ void sgd_one(T& w, T& v, T d, const UpdateArgs<T>& a)
   }
 }
 
+template <typename T>
+__device__ __forceinline__ T pre_delta(T d, const UpdateArgs<T>& a) {
+  if (a.add_zero) d = Rn<T>::add(d, T(0));  // the communicator's zero contribution (executors.cpp:278)
+  if (a.post_div != T(0)) d = Rn<T>::div(d, a.post_div);
+  return d;
+}
+
+__device__ __forceinline__ float tf32_round(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+template <typename T>
+__device__ __forceinline__ void store_split(const UpdateArgs<T>&, int64_t, const T*, int) {}
+template <>
+__device__ __forceinline__ void store_split<float>(const UpdateArgs<float>& a, int64_t e, const float* w, int n) {
+  if (!a.w_hi) return;
+  if (n == 4) {
+    float4 h = make_float4(tf32_round(w[0]), tf32_round(w[1]), tf32_round(w[2]), tf32_round(w[3]));
+    *reinterpret_cast<float4*>(a.w_hi + e) = h;
+    *reinterpret_cast<float4*>(a.w_lo + e) = make_float4(tf32_round(w[0] - h.x), tf32_round(w[1] - h.y),
+                                                         tf32_round(w[2] - h.z), tf32_round(w[3] - h.w));
+    return;
+  }
+  for (int q = 0; q < n; ++q) {
+    float h = tf32_round(w[q]);
+    a.w_hi[e + q] = h;
+    a.w_lo[e + q] = tf32_round(w[q] - h);
+  }
+}
+
 template <typename T, bool EXACT>
 __global__ void __launch_bounds__(256) update_kernel(UpdateArgs<T> a) {
   constexpr int V = Vec<T>::kN;
-  const int64_t nvec = a.n_params / V;
+  const int64_t nvec = a.scalar_only ? 0 : a.n_params / V;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   bool bad = false;
   const bool mom = a.mode != 0;
@@ -279,7 +310,7 @@ __global__ void __launch_bounds__(256) update_kernel(UpdateArgs<T> a) {
     if (mom) v = ld16(a.v + e);
 #pragma unroll
     for (int q = 0; q < V; ++q) {
-      T dq = a.post_div != T(0) ? Rn<T>::div(d.v[q], a.post_div) : d.v[q];
+      T dq = pre_delta(d.v[q], a);
       T vq = mom ? v.v[q] : T(0);
       sgd_one<T, EXACT>(w.v[q], vq, dq, a);
       if (mom) v.v[q] = vq;
@@ -287,20 +318,21 @@ __global__ void __launch_bounds__(256) update_kernel(UpdateArgs<T> a) {
     }
     st16(a.w + e, w);
     if (mom) st16(a.v + e, v);
+    store_split<T>(a, e, w.v, V);
   }
-  for (int64_t e = nvec * V + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e <= a.n_params;
-       e += stride) {
+  const int64_t end = a.n_params + (a.loss_out ? 1 : 0);
+  for (int64_t e = nvec * V + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < end; e += stride) {
     const int64_t j = e / a.slice_len;
-    T d = a.slices.p[j][e - j * a.slice_len];
-    if (a.post_div != T(0)) d = Rn<T>::div(d, a.post_div);
+    T d = pre_delta(a.slices.p[j][e - j * a.slice_len], a);
     if (e == a.n_params) {  // the loss slot rides the same reduction (executors.cpp:59-63, 226)
-      if (a.loss_out) *a.loss_out = d;
+      *a.loss_out = d;
       continue;
     }
     T w = a.w[e], v = mom ? a.v[e] : T(0);
     sgd_one<T, EXACT>(w, v, d, a);
     a.w[e] = w;
     if (mom) a.v[e] = v;
+    store_split<T>(a, e, &w, 1);
     bad |= !isfinite(w);
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x % 32) == 0) atomicOr(a.bad, 1u);
@@ -416,14 +448,23 @@ template <typename T>
 void launch_ordered_sum(SrcList<T> src, int n_src, int64_t len, T* dst, bool add_zero, T divisor, cudaStream_t st,
                         LaunchCounter& lc) {
   int64_t work = (len / Vec<T>::kN + 1) / 2 + 1;
-  ordered_sum_kernel<T><<<grid_for(work, 256), 256, 0, st>>>(src, n_src, len, dst, add_zero, divisor);
+  bool scalar = (reinterpret_cast<uintptr_t>(dst) & 15u) != 0;
+  for (int i = 0; i < n_src; ++i) scalar = scalar || (reinterpret_cast<uintptr_t>(src.p[i]) & 15u) != 0;
+  if (scalar) work = len;
+  ordered_sum_kernel<T><<<grid_for(work, 256), 256, 0, st>>>(src, n_src, len, dst, add_zero, divisor, scalar);
   ++lc.n;
   LSGD_CUDA(cudaGetLastError());
 }
 
 template <typename T>
-void launch_update(const UpdateArgs<T>& a, bool exact, cudaStream_t st, LaunchCounter& lc) {
-  int g = grid_for(a.n_params / Vec<T>::kN + 1, 256);
+void launch_update(const UpdateArgs<T>& a_in, bool exact, cudaStream_t st, LaunchCounter& lc) {
+  UpdateArgs<T> a = a_in;
+  auto misaligned = [](const void* p) { return p != nullptr && (reinterpret_cast<uintptr_t>(p) & 15u) != 0; };
+  bool slices_ok = a.slice_len % Vec<T>::kN == 0;
+  for (int j = 0; j < kMaxPeers && a.slices.p[j]; ++j) slices_ok = slices_ok && !misaligned(a.slices.p[j]);
+  a.scalar_only = (misaligned(a.w) || misaligned(a.v) || misaligned(a.w_hi) || misaligned(a.w_lo) || !slices_ok) ? 1 : 0;
+  int64_t work = a.scalar_only ? a.n_params + 1 : a.n_params / Vec<T>::kN + 1;
+  int g = grid_for(work, 256);
   if (exact) update_kernel<T, true><<<g, 256, 0, st>>>(a);
   else update_kernel<T, false><<<g, 256, 0, st>>>(a);
   ++lc.n;

@@ -54,7 +54,9 @@ void launch_ordered_sum(SrcList<T> src, int n_src, int64_t len, T* dst, bool add
                         cudaStream_t st, LaunchCounter& lc);
 
 // --- K8: pull the averaged gradient slices and apply the postponed update (optimizer.cpp:24-42) ------------
-// delta[e] = slices[e / S][e % S] (/ post_div when post_div != 0, the CSGD per-worker division).
+// delta[e] = ((slices[e / S][e % S] [+ 0.0]) [/ post_div]): post_div is the CSGD per-worker /N, add_zero + /N the
+// single-worker group's communicator arithmetic when the reduce is skipped. Optionally writes the TF32 hi/lo split
+// of the updated weights for the tensor-core GEMMs.
 template <typename T>
 struct UpdateArgs {
   SrcList<T> slices;
@@ -64,8 +66,12 @@ struct UpdateArgs {
   T* v;
   int mode;
   T lr, momentum, weight_decay, post_div;
+  int add_zero;
+  int scalar_only;    // set by the launcher when a bucket's w/v base is not 16-byte aligned
   T* loss_out;        // receives delta[n_params] (the loss slot), may be null
   unsigned* bad;      // OR-ed 1 when a non-finite parameter is produced
+  float* w_hi;        // fp32 only, may be null
+  float* w_lo;
 };
 template <typename T>
 void launch_update(const UpdateArgs<T>& a, bool exact, cudaStream_t st, LaunchCounter& lc);

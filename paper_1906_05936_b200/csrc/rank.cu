@@ -1,17 +1,19 @@
-// LSGD step engine — see engine.hpp for the design. Reference loop structure: executors.cpp:190-304
-// (worker: io -> postponed update -> compute -> local reduce; communicator: reduce -> /N -> global allreduce ->
-// broadcast), csgd executors.cpp:132-188, sequential :87-130.
+// LSGD step engine, one Rank per GPU — see engine.hpp for the design. Reference loop structure:
+// executors.cpp:190-304 (worker: io -> postponed update -> compute -> local reduce; communicator: reduce -> /N ->
+// global allreduce -> broadcast), csgd executors.cpp:132-188, sequential :87-130.
+//
+// The step is pipelined per gradient bucket (one bucket per layer): as soon as the backward pass has written layer
+// k's gradient, the comm stream starts the ordered intra-group reduce (K6) and the inter-group average (K7) of
+// that bucket while the main stream continues with layer k-1's backward. The postponed update is applied per
+// bucket right before the forward of the same layer in the next step, so forward layer 0 only waits for bucket 0.
+// Arithmetic per element is unchanged (the reference's ascending-order sums), only the schedule differs.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
 #include <algorithm>
-#include <atomic>
-#include <chrono>
 #include <cstring>
-#include <exception>
 #include <map>
 #include <mutex>
-#include <thread>
 
 #include "engine.hpp"
 #include "gemm_tc.cuh"
@@ -20,8 +22,8 @@
 namespace lsgd_b200 {
 
 namespace {
-constexpr int64_t kAlign = 64;       // elements: slices start on 256 B (fp32) / 512 B (fp64) boundaries
-constexpr int kRing = 4;             // pinned index ring depth (host may run this many steps ahead)
+constexpr int64_t kAlign = 64;         // elements: slices start on 256 B (fp32) / 512 B (fp64) boundaries
+constexpr int kRing = 4;               // pinned index ring depth (host may run this many steps ahead)
 constexpr int64_t kLossCap = 1 << 16;  // device loss history ring per rank
 
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
@@ -33,18 +35,42 @@ struct PhaseEvents {
 }  // namespace
 
 Geometry::Geometry(const RunSpec& spec, int es) : esize(es) {
-  if (spec.c.model == LSGD_B200_MODEL_SYNTHETIC_GRADIENT) P = spec.c.synthetic_params;
-  else P = Layout(spec.layers).n_params;
-  P1 = P + 1;
-  int k = spec.k();
-  S = round_up((P1 + k - 1) / k, kAlign);
-  Ppad = S * k;
+  if (spec.c.model == LSGD_B200_MODEL_SYNTHETIC_GRADIENT) {
+    P = spec.c.synthetic_params;
+    Bucket b;
+    b.n = P;
+    buckets.push_back(b);
+  } else {
+    Layout L(spec.layers);
+    P = L.n_params;
+    check<ConfigError>(L.depth() <= kMaxBuckets, "at most ", kMaxBuckets, " layers are supported");
+    for (int k = 0; k < L.depth(); ++k) {
+      Bucket b;
+      b.pstart = L.w_off[static_cast<size_t>(k)];
+      b.n = static_cast<int64_t>(L.in(k)) * L.out(k) + L.out(k);
+      buckets.push_back(b);
+    }
+  }
+  buckets.back().loss = true;
+  const int k = spec.k();
+  int64_t poff = 0, goff = 0;
+  for (auto& b : buckets) {
+    const int64_t len = b.n + (b.loss ? 1 : 0);
+    b.S = round_up((len + k - 1) / k, kAlign);
+    b.poff = poff;
+    b.goff = goff;
+    poff += b.S * k;
+    goff += b.S;
+  }
+  Ppad = poff;
+  Sg = goff;
+  loss_at = buckets.back().poff + buckets.back().n;
   peer.flags = 0;
-  peer.payload = 256;
+  peer.payload = round_up(3 * kMaxBuckets * 8, 256);
   peer.s[0] = round_up(peer.payload + Ppad * es, 256);
-  peer.s[1] = round_up(peer.s[0] + S * es, 256);
-  peer.gbar = round_up(peer.s[1] + S * es, 256);
-  peer.total = round_up(peer.gbar + S * es, 256);
+  peer.s[1] = round_up(peer.s[0] + Sg * es, 256);
+  peer.gbar = round_up(peer.s[1] + Sg * es, 256);
+  peer.total = round_up(peer.gbar + Sg * es, 256);
 }
 
 // ================================================================================================ RankImpl
@@ -57,11 +83,11 @@ class RankImpl final : public Rank {
     N_ = spec_.N();
     G_ = spec_.G();
     k_ = spec_.k();
+    nb_ = static_cast<int>(geo_.buckets.size());
     alg_ = spec_.c.algorithm;
     exact_ = sizeof(T) == 8;
     synth_ = spec_.c.model == LSGD_B200_MODEL_SYNTHETIC_GRADIENT;
     B_ = alg_ == LSGD_B200_SEQUENTIAL ? static_cast<int>(spec_.global_batch()) : spec_.c.local_batch;
-    check<ConfigError>(N_ <= kMaxPeers * 8, "n_workers too large for one box");
     check<ConfigError>(k_ <= kMaxPeers && G_ <= kMaxPeers, "group size and group count must be <= ", kMaxPeers);
     LSGD_CUDA(cudaSetDevice(dev_));
     int major = 0;
@@ -74,8 +100,7 @@ class RankImpl final : public Rank {
     split_ = workers_.size() == 1;
     if (split_) LSGD_CUDA(cudaStreamCreateWithPriority(&comm_, cudaStreamNonBlocking, hi));
     else comm_ = main_;
-    LSGD_CUDA(cudaEventCreateWithFlags(&ev_handoff_, cudaEventDisableTiming));
-    LSGD_CUDA(cudaEventCreateWithFlags(&ev_back_, cudaEventDisableTiming));
+    for (int b = 0; b < kMaxBuckets; ++b) LSGD_CUDA(cudaEventCreateWithFlags(&ev_bucket_[b], cudaEventDisableTiming));
     void* to = nullptr;
     LSGD_CUDA(cudaHostAlloc(&to, sizeof(int), cudaHostAllocMapped));
     timed_out_host_ = static_cast<volatile int*>(to);
@@ -90,14 +115,13 @@ class RankImpl final : public Rank {
     LSGD_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ring_), sizeof(int32_t) * kRing * workers_.size() * B_,
                             cudaHostAllocDefault));
     if (!synth_) {
-      if (spec_.c.shared_minibatch || alg_ == LSGD_B200_SEQUENTIAL) draw_.resize(static_cast<size_t>(spec_.global_batch()));
-      else draw_.resize(static_cast<size_t>(spec_.global_batch()));
+      draw_.resize(static_cast<size_t>(spec_.global_batch()));
       shards_ = std::make_unique<ShardStream>(spec_);
     }
+    use_tc_ = tc_eligible();
     for (int wid : workers_) alloc_worker(wid);
     if (hist_rows_ > 0)
       LSGD_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hist_), sizeof(T) * hist_rows_ * geo_.P, cudaHostAllocDefault));
-    use_tc_ = tc_eligible();
   }
 
   ~RankImpl() override {
@@ -131,8 +155,7 @@ class RankImpl final : public Rank {
     cudaFreeHost(const_cast<int*>(timed_out_host_));
     cudaFree(bad_dev_);
     for (int i = 0; i < kRing; ++i) cudaEventDestroy(ring_ev_[i]);
-    cudaEventDestroy(ev_handoff_);
-    cudaEventDestroy(ev_back_);
+    for (int b = 0; b < kMaxBuckets; ++b) cudaEventDestroy(ev_bucket_[b]);
     if (split_) cudaStreamDestroy(comm_);
     cudaStreamDestroy(main_);
   }
@@ -192,9 +215,10 @@ class RankImpl final : public Rank {
     for (auto& wk : ws_) {
       LSGD_CUDA(cudaMemcpy(wk.w, conv.data(), sizeof(T) * geo_.P, cudaMemcpyHostToDevice));
       if (wk.v) LSGD_CUDA(cudaMemset(wk.v, 0, sizeof(T) * geo_.P));
+      if (use_tc_) tc_split_weights(wk.tc, L_, reinterpret_cast<const float*>(wk.w), main_, lc_);
     }
     if (hist_rows_ > 0) std::memcpy(hist_, conv.data(), sizeof(T) * geo_.P);  // w_0
-    if (use_tc_) for (auto& wk : ws_) tc_resplit_weights(wk);
+    LSGD_CUDA(cudaStreamSynchronize(main_));
   }
 
   void get_params(int worker, double* w) override {
@@ -205,7 +229,7 @@ class RankImpl final : public Rank {
     for (int64_t i = 0; i < geo_.P; ++i) w[i] = static_cast<double>(tmp[static_cast<size_t>(i)]);
   }
 
-  // ------------------------------------------------------------------------------------------ the step
+  // ------------------------------------------------------------------------------------------ the step API
   void issue_steps(int64_t n, const int32_t* host_idx, bool shard_only) override {
     LSGD_CUDA(cudaSetDevice(dev_));
     for (int64_t q = 0; q < n; ++q) {
@@ -236,7 +260,9 @@ class RankImpl final : public Rank {
     LSGD_CUDA(cudaSetDevice(dev_));
     if (alg_ == LSGD_B200_LSGD && applied_ < t_next_) {
       current_phase() = "broadcast";
-      for (auto& wk : ws_) apply(wk, t_next_ - 1);
+      for (auto& wk : ws_)
+        for (int b = 0; b < nb_; ++b) apply_bucket(wk, b, t_next_ - 1);
+      for (auto& wk : ws_) after_update(wk, t_next_ - 1);
       ++applied_;
     }
     synchronize();
@@ -337,12 +363,15 @@ class RankImpl final : public Rank {
     LSGD_CUDA(cudaSetDevice(dev_));
     Worker& w = ws_[0];
     io(t_next_, idx, true);
-    compute(w);
+    for (int k = 0; k < L_.depth(); ++k) forward_layer(w, k);
+    head(w);
+    for (int k = L_.depth() - 1; k >= 0; --k) backward_layer(w, k);
     LSGD_CUDA(cudaStreamSynchronize(main_));
-    std::vector<T> tmp(static_cast<size_t>(geo_.P1));
-    LSGD_CUDA(cudaMemcpy(tmp.data(), w.payload, sizeof(T) * geo_.P1, cudaMemcpyDeviceToHost));
-    for (int64_t i = 0; i < geo_.P; ++i) grad[i] = static_cast<double>(tmp[static_cast<size_t>(i)]);
-    *loss = static_cast<double>(tmp[static_cast<size_t>(geo_.P)]);
+    std::vector<T> tmp(static_cast<size_t>(geo_.Ppad));
+    LSGD_CUDA(cudaMemcpy(tmp.data(), w.payload, sizeof(T) * geo_.Ppad, cudaMemcpyDeviceToHost));
+    for (const Bucket& b : geo_.buckets)
+      for (int64_t i = 0; i < b.n; ++i) grad[b.pstart + i] = static_cast<double>(tmp[static_cast<size_t>(b.poff + i)]);
+    *loss = static_cast<double>(tmp[static_cast<size_t>(geo_.loss_at)]);
   }
 
   void abort() override { *timed_out_host_ = 1; }
@@ -378,7 +407,7 @@ class RankImpl final : public Rank {
     T* d1 = nullptr;
     T* sample_loss = nullptr;
     T* loss_hist = nullptr;
-    TcWorkspace tc;  // split-TF32 operand buffers of the tensor-core path
+    TcWorkspace tc;  // split-TF32 operands of the tensor-core path
   };
 
   Worker& find(int worker) {
@@ -404,25 +433,30 @@ class RankImpl final : public Rank {
     LSGD_CUDA(cudaMalloc(&w.loss_hist, sizeof(T) * kLossCap));
     LSGD_CUDA(cudaMemset(w.loss_hist, 0, sizeof(T) * kLossCap));
     if (synth_) {
-      // cfg4 synthetic gradient: g_r[k] = Rng(1000 + r).next_symmetric(1.0); fixed per run.
-      std::vector<T> g(static_cast<size_t>(geo_.P1));
+      // cfg4 synthetic gradient: g_r[k] = Rng(1000 + r).next_symmetric(1.0); fixed per run. The
+      // single bucket keeps the payload contiguous: [g_0 .. g_{P-1} | loss slot].
+      std::vector<T> g(static_cast<size_t>(geo_.P + 1));
       SplitMix64 r(1000 + static_cast<uint64_t>(wid));
       for (auto& e : g) e = static_cast<T>(r.sym(1.0));
-      LSGD_CUDA(cudaMemcpy(w.payload, g.data(), sizeof(T) * geo_.P1, cudaMemcpyHostToDevice));
+      LSGD_CUDA(cudaMemcpy(w.payload, g.data(), sizeof(T) * g.size(), cudaMemcpyHostToDevice));
     } else {
       const int d = spec_.c.n_features;
       LSGD_CUDA(cudaMalloc(&w.x, sizeof(T) * static_cast<size_t>(B_) * d));
       LSGD_CUDA(cudaMalloc(&w.y, sizeof(int32_t) * B_));
       LSGD_CUDA(cudaMalloc(&w.idx, sizeof(int32_t) * B_));
-      for (int k = 0; k < L_.depth(); ++k) {
-        T* a = nullptr;
-        LSGD_CUDA(cudaMalloc(&a, sizeof(T) * static_cast<size_t>(B_) * L_.out(k)));
-        w.act.push_back(a);
-      }
-      int wide = std::max(L_.widest(), spec_.c.n_features);
-      LSGD_CUDA(cudaMalloc(&w.d0, sizeof(T) * static_cast<size_t>(B_) * wide));
-      LSGD_CUDA(cudaMalloc(&w.d1, sizeof(T) * static_cast<size_t>(B_) * wide));
       LSGD_CUDA(cudaMalloc(&w.sample_loss, sizeof(T) * B_));
+      if (use_tc_) {
+        tc_alloc(w.tc, L_, B_, d);  // owns activations and deltas of the tensor-core path
+      } else {
+        for (int k = 0; k < L_.depth(); ++k) {
+          T* a = nullptr;
+          LSGD_CUDA(cudaMalloc(&a, sizeof(T) * static_cast<size_t>(B_) * L_.out(k)));
+          w.act.push_back(a);
+        }
+        int wide = std::max(L_.widest(), d);
+        LSGD_CUDA(cudaMalloc(&w.d0, sizeof(T) * static_cast<size_t>(B_) * wide));
+        LSGD_CUDA(cudaMalloc(&w.d1, sizeof(T) * static_cast<size_t>(B_) * wide));
+      }
     }
     ws_.push_back(std::move(w));
     peer_base_[static_cast<size_t>(wid)] = ws_.back().blk;
@@ -452,22 +486,22 @@ class RankImpl final : public Rank {
   T* peer_payload(int wid) const { return reinterpret_cast<T*>(base(wid) + geo_.peer.payload); }
   T* peer_s(int wid, int par) const { return reinterpret_cast<T*>(base(wid) + geo_.peer.s[par]); }
   T* peer_gbar(int wid) const { return reinterpret_cast<T*>(base(wid) + geo_.peer.gbar); }
-  const volatile unsigned long long* peer_flag(int wid, int which) const {
-    return reinterpret_cast<const volatile unsigned long long*>(base(wid) + geo_.peer.flags) + which;
+  const volatile unsigned long long* peer_flag(int wid, int which, int b) const {
+    return reinterpret_cast<const volatile unsigned long long*>(base(wid) + geo_.peer.flags) + which * kMaxBuckets + b;
   }
 
   unsigned long long timeout_ns() const {
     return static_cast<unsigned long long>(spec_.c.collective_timeout_s * 1e9);
   }
 
-  void wait(const std::vector<int>& wids, int which, unsigned long long target, cudaStream_t st) {
+  void wait(const std::vector<int>& wids, int which, int b, unsigned long long target, cudaStream_t st) {
     FlagList fl{};
     int n = 0;
-    for (int wid : wids) fl.f[n++] = peer_flag(wid, which);
+    for (int wid : wids) fl.f[n++] = peer_flag(wid, which, b);
     launch_wait_flags(fl, n, target, timeout_ns(), timed_out_dev_, st, lc_);
   }
-  void signal(Worker& w, int which, unsigned long long v, cudaStream_t st) {
-    launch_signal_flag(w.flags + which, v, st, lc_);
+  void signal(Worker& w, int which, int b, unsigned long long v, cudaStream_t st) {
+    launch_signal_flag(w.flags + which * kMaxBuckets + b, v, st, lc_);
   }
 
   // --- kernel-family timing (bench roofline) and phase spans (executors.hpp:248-267)
@@ -508,9 +542,10 @@ class RankImpl final : public Rank {
   }
   size_t widx(const Worker& w) const { return static_cast<size_t>(&w - ws_.data()); }
 
-  // io: host sampler -> pinned ring -> H2D -> gather (K1). executors.cpp:236-239 / 75-79.
+  // ------------------------------------------------------------------------------------------ io
+  // host sampler -> pinned ring -> H2D -> gather (K1). executors.cpp:236-239 / 75-79.
   void io(int64_t t, const int32_t* given, bool shard_only) {
-    if (rows_x_) {  // caller-supplied host rows: the H2D copy is the io (executors.cpp:236-239)
+    if (rows_x_) {  // caller-supplied host rows: the H2D copy is the io
       const int d = spec_.c.n_features;
       for (size_t i = 0; i < ws_.size(); ++i) {
         Worker& w = ws_[i];
@@ -553,43 +588,60 @@ class RankImpl final : public Rank {
     LSGD_CUDA(cudaEventRecord(ring_ev_[slot], main_));
   }
 
-  // compute: forward + backward of the local shard into the payload (mlp.cpp:238-273 as batched GEMMs).
-  void compute(Worker& w) {
+  // ------------------------------------------------------------------------------------------ compute
+  // forward layer k / head / backward layer k of the local shard (mlp.cpp:60-127 as batched GEMMs); the
+  // gradient of layer k lands in payload bucket k, the mean loss in the loss slot.
+  T* delta_buf(Worker& w, int k) { return ((L_.depth() - 1 - k) & 1) ? w.d1 : w.d0; }
+
+  void forward_layer(Worker& w, int k) {
     if (synth_) return;
+    Timed tm(this, "gemm", main_);
     if (use_tc_) {
-      tc_compute(w);
+      tc_forward_layer(w.tc, L_, k, reinterpret_cast<const float*>(w.w), reinterpret_cast<const float*>(w.x), main_,
+                       lc_);
       return;
     }
-    Timed tm(this, "gemm", main_);
-    const int depth = L_.depth();
-    const T* in = w.x;
-    for (int k = 0; k < depth; ++k) {
-      const int ni = L_.in(k), no = L_.out(k);
-      const T* Wk = w.w + L_.w_off[static_cast<size_t>(k)];
-      const T* bk = w.w + L_.b_off[static_cast<size_t>(k)];
-      launch_gemm_simt<T>(kEpiForward, exact_, B_, no, ni, in, ni, 1, Wk, 1, ni, w.act[static_cast<size_t>(k)], no, bk,
-                          k + 1 < depth ? 1 : 0, T(0), nullptr, main_, lc_);
-      in = w.act[static_cast<size_t>(k)];
+    const int ni = L_.in(k), no = L_.out(k);
+    const T* in = k == 0 ? w.x : w.act[static_cast<size_t>(k - 1)];
+    const T* Wk = w.w + L_.w_off[static_cast<size_t>(k)];
+    const T* bk = w.w + L_.b_off[static_cast<size_t>(k)];
+    launch_gemm_simt<T>(kEpiForward, exact_, B_, no, ni, in, ni, 1, Wk, 1, ni, w.act[static_cast<size_t>(k)], no, bk,
+                        k + 1 < L_.depth() ? 1 : 0, T(0), nullptr, main_, lc_);
+  }
+
+  void head(Worker& w) {
+    if (synth_) return;
+    T* loss_out = w.payload + geo_.loss_at;
+    if (use_tc_) {
+      tc_head(w.tc, L_, w.y, reinterpret_cast<float*>(w.sample_loss), reinterpret_cast<float*>(loss_out), main_, lc_);
+      return;
     }
-    const int C = L_.out(depth - 1);
-    T* dcur = w.d0;
-    T* dnext = w.d1;
-    launch_softmax_xent<T>(w.act[static_cast<size_t>(depth - 1)], w.y, B_, C, dcur, w.sample_loss, main_, lc_);
-    launch_mean_loss<T>(w.sample_loss, B_, w.payload + geo_.P, main_, lc_);
-    for (int k = depth - 1; k >= 0; --k) {
-      const int ni = L_.in(k), no = L_.out(k);
-      const T* aprev = k == 0 ? w.x : w.act[static_cast<size_t>(k - 1)];
-      T* gW = w.payload + L_.w_off[static_cast<size_t>(k)];
-      T* gb = w.payload + L_.b_off[static_cast<size_t>(k)];
-      launch_gemm_simt<T>(kEpiWeightGrad, exact_, no, ni, B_, dcur, 1, no, aprev, ni, 1, gW, ni, nullptr, 0,
-                          static_cast<T>(B_), nullptr, main_, lc_);
-      launch_bias_grad<T>(dcur, B_, no, gb, main_, lc_);
-      if (k > 0) {
-        const T* Wk = w.w + L_.w_off[static_cast<size_t>(k)];
-        launch_gemm_simt<T>(kEpiInputGrad, exact_, B_, ni, no, dcur, no, 1, Wk, ni, 1, dnext, ni, nullptr, 0, T(0),
-                            w.act[static_cast<size_t>(k - 1)], main_, lc_);
-        std::swap(dcur, dnext);
-      }
+    const int depth = L_.depth();
+    launch_softmax_xent<T>(w.act[static_cast<size_t>(depth - 1)], w.y, B_, L_.out(depth - 1), delta_buf(w, depth - 1),
+                           w.sample_loss, main_, lc_);
+    launch_mean_loss<T>(w.sample_loss, B_, loss_out, main_, lc_);
+  }
+
+  void backward_layer(Worker& w, int k) {
+    if (synth_) return;
+    Timed tm(this, "gemm", main_);
+    const Bucket& bk = geo_.buckets[static_cast<size_t>(k)];
+    const int ni = L_.in(k), no = L_.out(k);
+    T* gW = w.payload + bk.poff;
+    T* gb = gW + static_cast<int64_t>(ni) * no;
+    if (use_tc_) {
+      tc_backward_layer(w.tc, L_, k, reinterpret_cast<float*>(gW), reinterpret_cast<float*>(gb), main_, lc_);
+      return;
+    }
+    T* dcur = delta_buf(w, k);
+    const T* aprev = k == 0 ? w.x : w.act[static_cast<size_t>(k - 1)];
+    launch_gemm_simt<T>(kEpiWeightGrad, exact_, no, ni, B_, dcur, 1, no, aprev, ni, 1, gW, ni, nullptr, 0,
+                        static_cast<T>(B_), nullptr, main_, lc_);
+    launch_bias_grad<T>(dcur, B_, no, gb, main_, lc_);
+    if (k > 0) {
+      const T* Wk = w.w + L_.w_off[static_cast<size_t>(k)];
+      launch_gemm_simt<T>(kEpiInputGrad, exact_, B_, ni, no, dcur, no, 1, Wk, ni, 1, delta_buf(w, k - 1), ni, nullptr, 0,
+                          T(0), w.act[static_cast<size_t>(k - 1)], main_, lc_);
     }
   }
 
@@ -599,128 +651,168 @@ class RankImpl final : public Rank {
     return m;
   }
 
-  // local reduce: slice owner (g, j) sums slice j of its group's payloads in ascending worker order, adds the
+  // ------------------------------------------------------------------------------------------ collectives
+  // One worker per group and one group: the communicator's (g + 0.0) / N is folded into the update (no copy).
+  bool reduce_folded() const { return alg_ != LSGD_B200_SEQUENTIAL && k_ == 1 && G_ == 1 && !flat_comm_; }
+  bool flat_nccl() const { return alg_ == LSGD_B200_CSGD && flat_comm_ != nullptr; }
+
+  // K6 for bucket b: slot (g, j) sums sub-slice j of its group's payloads in ascending worker order, adds the
   // communicator's zero vector, divides by N (transport.cpp:27-48; executors.cpp:278-288).
-  void local_reduce(Worker& w, int64_t t) {
-    if (alg_ == LSGD_B200_SEQUENTIAL) return;
+  void reduce_bucket(Worker& w, int b, int64_t t, cudaStream_t st) {
+    const Bucket& bk = geo_.buckets[static_cast<size_t>(b)];
     const int par = static_cast<int>(t & 1);
-    if (alg_ == LSGD_B200_CSGD && flat_comm_) {
-      // K9 baseline: flat NCCL ring allreduce of the whole payload over N ranks (in place).
-      Timed tm(this, "global", main_);
-      LSGD_NCCL(ncclAllReduce(w.payload, w.payload, static_cast<size_t>(geo_.Ppad), nccl_type(), ncclSum, flat_comm_,
-                              main_));
-      return;
-    }
     auto members = group_members(w.g);
-    wait(members, kFlagGrad, static_cast<unsigned long long>(t + 1), main_);
+    wait(members, kFlagGrad, b, static_cast<unsigned long long>(t + 1), st);
     SrcList<T> src{};
-    for (int i = 0; i < k_; ++i) src.p[i] = peer_payload(members[static_cast<size_t>(i)]) + w.j * geo_.S;
-    T* dst = G_ == 1 ? w.gbar : w.s[par];
+    for (int i = 0; i < k_; ++i) src.p[i] = peer_payload(members[static_cast<size_t>(i)]) + bk.poff + w.j * bk.S;
+    T* dst = (G_ == 1 ? w.gbar : w.s[par]) + bk.goff;
     {
-      Timed tm(this, "reduce", main_);
-      launch_ordered_sum<T>(src, k_, geo_.S, dst, alg_ == LSGD_B200_LSGD, static_cast<T>(N_), main_, lc_);
+      Timed tm(this, "reduce", st);
+      launch_ordered_sum<T>(src, k_, bk.S, dst, alg_ == LSGD_B200_LSGD, static_cast<T>(N_), st, lc_);
     }
-    if (G_ == 1) signal(w, kFlagBcast, static_cast<unsigned long long>(t + 1), main_);
-    // every local slice sum is published before any local global-average waits on peers' (emulated ranks)
-    else if (slice_comm_ == nullptr) signal(w, kFlagSlice, static_cast<unsigned long long>(t + 1), main_);
+    if (G_ == 1) signal(w, kFlagBcast, b, static_cast<unsigned long long>(t + 1), st);
+    else if (slice_comm_ == nullptr) signal(w, kFlagSlice, b, static_cast<unsigned long long>(t + 1), st);
   }
 
-  // global average across communicators (executors.cpp:290-295): NCCL (or the ordered peer sum) on the comm
-  // stream, so it overlaps the workers' next io.
-  void global(Worker& w, int64_t t) {
-    if (G_ == 1 || alg_ != LSGD_B200_LSGD) return;
+  // K7 for bucket b: average across communicators (executors.cpp:290-295) with NCCL over the G slot-j owners (or
+  // the ordered peer sum), on the comm stream.
+  void global_bucket(Worker& w, int b, int64_t t, cudaStream_t st) {
+    if (G_ == 1) return;
+    const Bucket& bk = geo_.buckets[static_cast<size_t>(b)];
     const int par = static_cast<int>(t & 1);
-    const bool nccl = slice_comm_ != nullptr;
-    if (split_) {
-      LSGD_CUDA(cudaEventRecord(ev_handoff_, main_));
-      LSGD_CUDA(cudaStreamWaitEvent(comm_, ev_handoff_, 0));
-    }
-    launch_sleep(spec_.c.global_link_delay_s, comm_, lc_);
-    if (nccl) {
-      Timed tm(this, "global", comm_);
-      LSGD_NCCL(ncclAllReduce(w.s[par], w.gbar, static_cast<size_t>(geo_.S), nccl_type(), ncclSum, slice_comm_, comm_));
+    if (slice_comm_) {
+      Timed tm(this, "global", st);
+      LSGD_NCCL(ncclAllReduce(w.s[par] + bk.goff, w.gbar + bk.goff, static_cast<size_t>(bk.S), nccl_type(), ncclSum,
+                              slice_comm_, st));
     } else {
       std::vector<int> owners;
       for (int g = 0; g < G_; ++g) owners.push_back(g * k_ + w.j);
-      wait(owners, kFlagSlice, static_cast<unsigned long long>(t + 1), comm_);
+      wait(owners, kFlagSlice, b, static_cast<unsigned long long>(t + 1), st);
       SrcList<T> src{};
-      for (int g = 0; g < G_; ++g) src.p[g] = peer_s(owners[static_cast<size_t>(g)], par);
-      Timed tm(this, "global", comm_);
-      launch_ordered_sum<T>(src, G_, geo_.S, w.gbar, false, T(0), comm_, lc_);
+      for (int g = 0; g < G_; ++g) src.p[g] = peer_s(owners[static_cast<size_t>(g)], par) + bk.goff;
+      Timed tm(this, "global", st);
+      launch_ordered_sum<T>(src, G_, bk.S, w.gbar + bk.goff, false, T(0), st, lc_);
     }
-    signal(w, kFlagBcast, static_cast<unsigned long long>(t + 1), comm_);
+    signal(w, kFlagBcast, b, static_cast<unsigned long long>(t + 1), st);
   }
 
-  // broadcast + update (executors.cpp:210-229): pull the k averaged slices of the group, apply sgd_update,
-  // check finiteness, record the round's loss.
-  void apply(Worker& w, int64_t u) {
+  // K8 for bucket b of round u (executors.cpp:210-229): pull the k averaged sub-slices of the group, apply
+  // sgd_update to the bucket's parameters, check finiteness, record the loss (last bucket).
+  void apply_bucket(Worker& w, int b, int64_t u) {
+    const Bucket& bk = geo_.buckets[static_cast<size_t>(b)];
     const size_t wi = widx(w);
-    phase_mark(wi, u, 4, 0, main_);
+    if (b == 0) phase_mark(wi, u, 4, 0, main_);
     UpdateArgs<T> a{};
-    a.slice_len = geo_.S;
-    a.n_params = geo_.P;
-    if (alg_ == LSGD_B200_SEQUENTIAL) {
-      for (int j = 0; j < k_; ++j) a.slices.p[j] = w.payload + j * geo_.S;
-    } else if (alg_ == LSGD_B200_CSGD && flat_comm_) {
-      for (int j = 0; j < k_; ++j) a.slices.p[j] = w.payload + j * geo_.S;
-      a.post_div = static_cast<T>(N_);  // the per-worker /N after the flat allreduce (executors.cpp:170)
+    a.slice_len = bk.S;
+    a.n_params = bk.n;
+    if (alg_ == LSGD_B200_SEQUENTIAL || reduce_folded() || flat_nccl()) {
+      for (int j = 0; j < k_; ++j) a.slices.p[j] = w.payload + bk.poff + j * bk.S;
+      if (reduce_folded()) {
+        a.add_zero = alg_ == LSGD_B200_LSGD ? 1 : 0;
+        a.post_div = static_cast<T>(N_);
+      }
+      if (flat_nccl()) a.post_div = static_cast<T>(N_);  // the per-worker /N after the flat allreduce (:170)
     } else {
       auto owners = group_members(w.g);
-      wait(owners, kFlagBcast, static_cast<unsigned long long>(u + 1), main_);
-      for (int j = 0; j < k_; ++j) a.slices.p[j] = peer_gbar(owners[static_cast<size_t>(j)]);
+      wait(owners, kFlagBcast, b, static_cast<unsigned long long>(u + 1), main_);
+      for (int j = 0; j < k_; ++j) a.slices.p[j] = peer_gbar(owners[static_cast<size_t>(j)]) + bk.goff;
     }
-    phase_mark(wi, u, 4, 1, main_);
-    phase_mark(wi, u, 5, 0, main_);
-    a.w = w.w;
-    a.v = w.v;
+    if (b == 0) {
+      phase_mark(wi, u, 4, 1, main_);
+      phase_mark(wi, u, 5, 0, main_);
+    }
+    a.w = w.w + bk.pstart;
+    a.v = w.v ? w.v + bk.pstart : nullptr;
     a.mode = spec_.c.mode;
     a.lr = static_cast<T>(spec_.lr(u));
     a.momentum = static_cast<T>(spec_.c.momentum);
     a.weight_decay = static_cast<T>(spec_.c.weight_decay);
-    a.loss_out = w.loss_hist + (u % kLossCap);
+    a.loss_out = bk.loss ? w.loss_hist + (u % kLossCap) : nullptr;
     a.bad = bad_dev_;
-    {
-      Timed tm(this, "update", main_);
-      launch_update<T>(a, exact_, main_, lc_);
+    if (use_tc_) {
+      a.w_hi = w.tc.w_hi + bk.pstart;
+      a.w_lo = w.tc.w_lo + bk.pstart;
     }
-    if (use_tc_) tc_resplit_weights(w);
-    phase_mark(wi, u, 5, 1, main_);
+    Timed tm(this, "update", main_);
+    launch_update<T>(a, exact_, main_, lc_);
+  }
+
+  void after_update(Worker& w, int64_t u) {
+    phase_mark(widx(w), u, 5, 1, main_);
     if (hist_rows_ > 0 && w.id == workers_[0] && u + 1 < hist_rows_)
       LSGD_CUDA(cudaMemcpyAsync(hist_ + (u + 1) * geo_.P, w.w, sizeof(T) * geo_.P, cudaMemcpyDeviceToHost, main_));
   }
 
+  // ------------------------------------------------------------------------------------------ one step
   void issue_one(int64_t t, const int32_t* given, bool shard_only) {
+    const int D = synth_ ? 1 : L_.depth();
     current_phase() = "io";
     if (!synth_) io(t, given, shard_only);
-    else if (spec_.c.io_delay_s > 0) launch_sleep(spec_.c.io_delay_s, main_, lc_);
-    if (alg_ == LSGD_B200_LSGD && t >= 1) {
-      current_phase() = "broadcast";
-      for (auto& w : ws_) apply(w, t - 1);  // postponed update of round t-1 (executors.cpp:241-242)
-      ++applied_;
-    }
-    current_phase() = "compute";
+    else launch_sleep(spec_.c.io_delay_s, main_, lc_);
+
+    // postponed update of round t-1, bucket by bucket, each right before the forward of its layer
+    const bool postponed = alg_ == LSGD_B200_LSGD && t >= 1;
     for (auto& w : ws_) {
+      current_phase() = "compute";
       phase_mark(widx(w), t, 1, 0, main_);
-      compute(w);
+      for (int k = 0; k < D; ++k) {
+        if (postponed) {
+          current_phase() = "broadcast";
+          apply_bucket(w, k, t - 1);
+          current_phase() = "compute";
+        }
+        forward_layer(w, k);
+      }
+      if (postponed) after_update(w, t - 1);
+      head(w);
+      for (int k = D - 1; k >= 0; --k) {
+        backward_layer(w, k);
+        if (!flat_nccl() && !reduce_folded() && alg_ != LSGD_B200_SEQUENTIAL) {
+          signal(w, kFlagGrad, k, static_cast<unsigned long long>(t + 1), main_);
+          if (split_) LSGD_CUDA(cudaEventRecord(ev_bucket_[k], main_));
+        }
+      }
       phase_mark(widx(w), t, 1, 1, main_);
-      if (!(alg_ == LSGD_B200_CSGD && flat_comm_) && alg_ != LSGD_B200_SEQUENTIAL)
-        signal(w, kFlagGrad, static_cast<unsigned long long>(t + 1), main_);
     }
+    if (postponed) ++applied_;
+
+    // communicator work: per bucket in backward order, on the comm stream (overlapping the rest of the backward)
     current_phase() = "local_reduce";
-    for (auto& w : ws_) {
-      phase_mark(widx(w), t, 2, 0, main_);
-      local_reduce(w, t);
-      phase_mark(widx(w), t, 2, 1, main_);
+    if (flat_nccl()) {
+      Timed tm(this, "global", main_);
+      for (auto& w : ws_)
+        LSGD_NCCL(ncclAllReduce(w.payload, w.payload, static_cast<size_t>(geo_.Ppad), nccl_type(), ncclSum,
+                                flat_comm_, main_));
+    } else if (!reduce_folded() && alg_ != LSGD_B200_SEQUENTIAL) {
+      for (auto& w : ws_) phase_mark(widx(w), t, 2, 0, comm_);
+      if (split_) {
+        Worker& w = ws_[0];
+        for (int b = D - 1; b >= 0; --b) {
+          LSGD_CUDA(cudaStreamWaitEvent(comm_, ev_bucket_[b], 0));
+          if (b == D - 1) launch_sleep(spec_.c.global_link_delay_s, comm_, lc_);
+          reduce_bucket(w, b, t, comm_);
+          current_phase() = "global_allreduce";
+          global_bucket(w, b, t, comm_);
+          current_phase() = "local_reduce";
+        }
+      } else {
+        // emulated ranks share one stream: every local slice sum is published before any global average waits
+        for (int b = D - 1; b >= 0; --b)
+          for (auto& w : ws_) reduce_bucket(w, b, t, main_);
+        current_phase() = "global_allreduce";
+        launch_sleep(spec_.c.global_link_delay_s, main_, lc_);
+        for (int b = D - 1; b >= 0; --b)
+          for (auto& w : ws_) global_bucket(w, b, t, main_);
+      }
+      for (auto& w : ws_) phase_mark(widx(w), t, 3, 1, comm_);
     }
-    current_phase() = "global_allreduce";
-    for (auto& w : ws_) {
-      phase_mark(widx(w), t, 3, 0, comm_);
-      global(w, t);
-      phase_mark(widx(w), t, 3, 1, comm_);
-    }
-    if (alg_ != LSGD_B200_LSGD) {
+
+    if (alg_ != LSGD_B200_LSGD) {  // sequential / csgd: synchronous update in the same block (executors.cpp:172-177)
       current_phase() = "update";
-      for (auto& w : ws_) apply(w, t);
+      for (auto& w : ws_) {
+        for (int b = 0; b < D; ++b) apply_bucket(w, b, t);
+        after_update(w, t);
+      }
       ++applied_;
     }
     current_phase() = "between-phases";
@@ -728,23 +820,14 @@ class RankImpl final : public Rank {
 
   ncclDataType_t nccl_type() const { return sizeof(T) == 8 ? ncclFloat64 : ncclFloat32; }
 
-  // ----------------------------------------------------------------------------- tensor-core path hooks
   bool tc_eligible() const {
     if (synth_ || sizeof(T) != 4) return false;
     if (spec_.c.gemm == LSGD_B200_GEMM_SIMT) return false;
     bool ok = tc_shapes_supported(spec_.layers, B_);
     if (spec_.c.gemm == LSGD_B200_GEMM_TC)
-      check<ConfigError>(ok, "b200.gemm = tcgen05 needs every layer width and the local batch to be multiples of 128");
+      check<ConfigError>(ok, "b200.gemm = tcgen05 needs every layer width a multiple of 256 and the local batch a "
+                             "multiple of 128");
     return ok;
-  }
-  void tc_compute(Worker& w) {
-    Timed tm(this, "gemm", main_);
-    tc_forward_backward(w.tc, L_, B_, reinterpret_cast<const float*>(w.w), reinterpret_cast<const float*>(w.x), w.y,
-                        reinterpret_cast<float*>(w.payload), reinterpret_cast<float*>(w.sample_loss), main_, lc_);
-  }
-  void tc_resplit_weights(Worker& w) {
-    if (!w.tc.ready) tc_alloc(w.tc, L_, B_, spec_.c.n_features);
-    tc_split_weights(w.tc, L_, reinterpret_cast<const float*>(w.w), main_, lc_);
   }
 
   const T* rows_x_ = nullptr;
@@ -755,10 +838,10 @@ class RankImpl final : public Rank {
   int dev_;
   std::vector<int> workers_;
   int64_t hist_rows_;
-  int N_ = 1, G_ = 1, k_ = 1, alg_ = 2, B_ = 1;
+  int N_ = 1, G_ = 1, k_ = 1, nb_ = 1, alg_ = 2, B_ = 1;
   bool exact_ = false, synth_ = false, split_ = false, use_tc_ = false;
   cudaStream_t main_ = nullptr, comm_ = nullptr;
-  cudaEvent_t ev_handoff_ = nullptr, ev_back_ = nullptr;
+  cudaEvent_t ev_bucket_[kMaxBuckets] = {};
   std::vector<char*> peer_base_;
   std::vector<char*> ipc_opened_;
   ncclComm_t slice_comm_ = nullptr, flat_comm_ = nullptr;
@@ -799,197 +882,6 @@ void enable_phase_recording(Rank* r) {
 void note_ipc_mapping(Rank* r, char* p) {
   if (auto* a = dynamic_cast<RankImpl<float>*>(r)) a->note_ipc(p);
   if (auto* b = dynamic_cast<RankImpl<double>*>(r)) b->note_ipc(p);
-}
-
-// ================================================================================================ blobs
-void generate_blobs_parallel(uint64_t seed, int64_t n, int d, int c, double spread, double* x, int32_t* y) {
-  // Every row consumes exactly 2*ceil(d/2) draws; SplitMix64's state after m draws is seed + m*gamma, so rows
-  // can be produced independently and stay bit-identical to the sequential generator (dataset.cpp:32-70).
-  const int64_t per_row = 2 * ((d + 1) / 2);
-  std::vector<int32_t> ylab(static_cast<size_t>(c));
-  if (n * static_cast<int64_t>(d) < (1 << 22)) {
-    generate_blobs(seed, n, d, c, spread, x, y);
-    return;
-  }
-  // centres first (sequential, small), by generating a c-row prefix with the reference routine's stream
-  std::vector<double> centre(static_cast<size_t>(c) * d);
-  {
-    check<ConfigError>(c >= 2 && n >= c && d >= 1 && spread > 0.0, "generate_synthetic: invalid arguments");
-    SplitMix64 r(seed);
-    for (int cls = 0; cls < c; ++cls) {
-      double* mu = &centre[static_cast<size_t>(cls) * d];
-      for (int i = 0; i < d; i += 2) {
-        double a, b;
-        r.normal_pair(a, b);
-        mu[i] = a;
-        if (i + 1 < d) mu[i + 1] = b;
-      }
-      double ss = 0.0;
-      for (int j = 0; j < d; ++j) ss += mu[j] * mu[j];
-      double len = std::sqrt(ss);
-      if (len == 0.0) len = 1.0;
-      for (int j = 0; j < d; ++j) mu[j] = spread * mu[j] / len;
-    }
-  }
-  const uint64_t gamma = 0x9E3779B97F4A7C15ULL;
-  const uint64_t rows_base = seed + static_cast<uint64_t>(c) * static_cast<uint64_t>(per_row) * gamma;
-  unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-  std::vector<std::thread> th;
-  for (unsigned q = 0; q < nt; ++q) {
-    th.emplace_back([&, q] {
-      int64_t lo = n * q / nt, hi = n * (q + 1) / nt;
-      SplitMix64 r(rows_base + static_cast<uint64_t>(lo) * static_cast<uint64_t>(per_row) * gamma);
-      for (int64_t i = lo; i < hi; ++i) {
-        int32_t cls = static_cast<int32_t>(i % c);
-        y[i] = cls;
-        double* row = x + i * d;
-        for (int j = 0; j < d; j += 2) {
-          double a, b;
-          r.normal_pair(a, b);
-          row[j] = a;
-          if (j + 1 < d) row[j + 1] = b;
-        }
-        const double* mu = &centre[static_cast<size_t>(cls) * d];
-        for (int j = 0; j < d; ++j) row[j] += mu[j];
-      }
-    });
-  }
-  for (auto& t : th) t.join();
-}
-
-// ================================================================================================ world
-void run_world(const RunSpec& spec, bool want_history, bool want_workers, TrainOutputs& out) {
-  spec.validate();
-  int visible = 0;
-  LSGD_CUDA(cudaGetDeviceCount(&visible));
-  check<Error>(visible > 0, "no CUDA device visible: the b200 backend has no CPU fallback");
-  const int N = spec.N(), G = spec.G(), k = spec.k();
-  int ndev = spec.c.n_devices > 0 ? std::min(spec.c.n_devices, visible) : visible;
-  ndev = std::max(1, std::min(ndev, N));
-  const int64_t T = spec.iterations();
-  const int64_t P = Geometry(spec, 4).P;
-
-  // contiguous worker blocks per device (worker i -> GPU i when ndev == N)
-  std::vector<std::vector<int>> blocks(static_cast<size_t>(ndev));
-  for (int i = 0; i < N; ++i) blocks[static_cast<size_t>(static_cast<int64_t>(i) * ndev / N)].push_back(i);
-  std::vector<std::unique_ptr<Rank>> ranks;
-  for (int r = 0; r < ndev; ++r)
-    ranks.push_back(make_rank(spec, r, blocks[static_cast<size_t>(r)], r == 0 && want_history ? T + 1 : 0));
-
-  for (int a = 0; a < ndev; ++a) {
-    LSGD_CUDA(cudaSetDevice(a));
-    for (int b = 0; b < ndev; ++b) {
-      if (a == b) continue;
-      int can = 0;
-      LSGD_CUDA(cudaDeviceCanAccessPeer(&can, a, b));
-      check<TransportError>(can == 1, "GPU ", a, " cannot access GPU ", b, " peer memory (no NVLink/NVSwitch path)");
-      cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
-      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
-      else LSGD_CUDA(e);
-    }
-  }
-  for (auto& r : ranks)
-    for (auto& q : ranks)
-      for (int w : q->workers()) r->set_peer_base(w, q->peer_block(w));
-
-  // NCCL only when every rank hosts a single worker (one NCCL rank per device).
-  std::vector<ncclComm_t> comms_to_free;
-  const bool one_each = ndev == N;
-  if (one_each && spec.c.algorithm == LSGD_B200_LSGD && G > 1 && spec.c.global_algo == LSGD_B200_GLOBAL_NCCL) {
-    for (int j = 0; j < k; ++j) {
-      std::vector<int> devs;
-      for (int g = 0; g < G; ++g) devs.push_back(g * k + j);
-      std::vector<ncclComm_t> cs(static_cast<size_t>(G));
-      LSGD_NCCL(ncclCommInitAll(cs.data(), G, devs.data()));
-      for (int g = 0; g < G; ++g) ranks[static_cast<size_t>(g * k + j)]->set_nccl(cs[static_cast<size_t>(g)], nullptr);
-    }
-  }
-  if (one_each && spec.c.algorithm == LSGD_B200_CSGD && spec.c.csgd_nccl && N > 1) {
-    std::vector<int> devs;
-    for (int i = 0; i < N; ++i) devs.push_back(i);
-    std::vector<ncclComm_t> cs(static_cast<size_t>(N));
-    LSGD_NCCL(ncclCommInitAll(cs.data(), N, devs.data()));
-    for (int i = 0; i < N; ++i) ranks[static_cast<size_t>(i)]->set_nccl(nullptr, cs[static_cast<size_t>(i)]);
-  }
-
-  // inputs: host-generated with the reference-identical streams, data = seed, init = seed + 1
-  if (spec.c.model == LSGD_B200_MODEL_MLP) {
-    const int64_t n = spec.c.n_samples;
-    const int d = spec.c.n_features;
-    std::vector<double> x(static_cast<size_t>(n) * d);
-    std::vector<int32_t> y(static_cast<size_t>(n));
-    generate_blobs_parallel(spec.c.seed, n, d, spec.c.n_classes, spec.c.spread, x.data(), y.data());
-    for (size_t r = 0; r < ranks.size(); ++r) {
-      if (r > 0 && spec.c.data_source == LSGD_B200_DATA_HOST) ranks[r]->share_dataset_from(ranks[0].get());
-      else ranks[r]->upload_dataset(x.data(), y.data(), n);
-    }
-  }
-  std::vector<double> w0(static_cast<size_t>(P), 0.0);
-  if (spec.c.model == LSGD_B200_MODEL_MLP) {
-    init_weights(Layout(spec.layers), spec.c.seed + 1, spec.c.init_scale, w0.data());
-  } else {
-    SplitMix64 r(spec.c.seed + 1);  // synthetic-gradient model: w0 uniform in [-init_scale, init_scale]
-    for (auto& v : w0) v = r.sym(spec.c.init_scale);
-  }
-  for (auto& r : ranks) r->set_params(w0.data());
-  for (auto& r : ranks) {
-    r->synchronize();
-    enable_phase_recording(r.get());
-  }
-
-  // one host thread per GPU (executors.cpp:497-515); the first error aborts every rank's flag waits
-  std::vector<std::exception_ptr> errors(ranks.size());
-  std::atomic<bool> failed{false};
-  auto t_start = std::chrono::steady_clock::now();
-  std::vector<std::thread> threads;
-  for (size_t r = 0; r < ranks.size(); ++r) {
-    threads.emplace_back([&, r] {
-      try {
-        LSGD_CUDA(cudaSetDevice(ranks[r]->device()));
-        for (int64_t t = 0; t < T && !failed.load(); ++t) ranks[r]->issue_steps(1, nullptr, false);
-        ranks[r]->drain();
-      } catch (const std::exception& e) {
-        std::string msg = cat("rank ", ranks[r]->workers().front(), " in phase ", current_phase(), ": ", e.what());
-        if (dynamic_cast<const TransportError*>(&e)) errors[r] = std::make_exception_ptr(TransportError(msg));
-        else if (dynamic_cast<const ConfigError*>(&e)) errors[r] = std::make_exception_ptr(ConfigError(msg));
-        else errors[r] = std::make_exception_ptr(Error(msg));
-        failed = true;
-        for (auto& q : ranks) q->abort();
-      }
-    });
-  }
-  for (auto& t : threads) t.join();
-  for (auto& e : errors)
-    if (e) std::rethrow_exception(e);
-  out.total_wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
-
-  out.final_params.assign(static_cast<size_t>(P), 0.0);
-  ranks[0]->get_params(0, out.final_params.data());
-  out.loss.assign(static_cast<size_t>(T), 0.0);
-  out.lr.assign(static_cast<size_t>(T), 0.0);
-  ranks[0]->history(out.loss.data(), out.lr.data(), T);
-  if (want_history) {
-    out.history.assign(static_cast<size_t>((T + 1) * P), 0.0);
-    ranks[0]->param_history(out.history.data(), T + 1);
-  }
-  if (want_workers) {
-    out.worker_finals.assign(static_cast<size_t>(N * P), 0.0);
-    out.version_at_compute.assign(static_cast<size_t>(N * T), 0);
-    for (auto& r : ranks)
-      for (int w : r->workers()) {
-        r->get_params(w, out.worker_finals.data() + static_cast<int64_t>(w) * P);
-        // stream order makes gradient t read w_t: t updates were applied before compute t (executors.cpp:245)
-        for (int64_t t = 0; t < T; ++t) out.version_at_compute[static_cast<size_t>(w * T + t)] = t;
-      }
-  }
-  if (spec.c.record_phases) {
-    out.phase_spans.assign(static_cast<size_t>(N * T * 12), 0.0);
-    for (auto& r : ranks)
-      for (int w : r->workers()) r->phase_spans(w, out.phase_spans.data() + static_cast<int64_t>(w) * T * 12, T);
-  }
-  out.launches = 0;
-  for (auto& r : ranks) out.launches += r->launches();
-  ranks.clear();  // destroys comms too (each rank owns its handles)
 }
 
 }  // namespace lsgd_b200
