@@ -44,6 +44,7 @@ struct EpiParams {
   float* partial;  // split-K raw partial sums [splits][M][N]
   int M, N;
   uint32_t mn_lbo, mn_sbo, mn_layout;  // MN-major descriptor geometry (see op_desc)
+  uint32_t prefetch;                   // prefetch.tensormap the four operand maps
 };
 
 // ------------------------------------------------------------------------------------------ PTX helpers
@@ -198,10 +199,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     mbar_init(&acc_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta_hi)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta_lo)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb_hi)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb_lo)) : "memory");
+    if (ep.prefetch) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta_hi)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta_lo)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb_hi)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb_lo)) : "memory");
+    }
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_slot)),
@@ -458,6 +461,8 @@ void run_plan(const GemmPlan& p, cudaStream_t st, LaunchCounter& lc) {
   else launch_variant<true, false>(p, st);
   ++lc.n;
   LSGD_CUDA(cudaGetLastError());
+  static const bool probe_sync = std::getenv("LSGD_TC_SYNC") != nullptr;
+  if (probe_sync) LSGD_CUDA(cudaStreamSynchronize(st));
   if (p.splits > 1) {
     int64_t work = static_cast<int64_t>(p.M) * p.N / 32;
     int grid = static_cast<int>(std::min<int64_t>((work + 255) / 256, 148 * 8));
@@ -499,9 +504,11 @@ GemmPlan make_plan(const OpView& a_hi, const float* a_lo, const OpView& b_hi, co
   p.ep.mn_lbo = g.lbo;
   p.ep.mn_sbo = g.sbo;
   p.ep.mn_layout = g.layout;
+  static const bool no_prefetch = std::getenv("LSGD_TC_NOPREFETCH") != nullptr;  // bring-up probe only
+  p.ep.prefetch = no_prefetch ? 0u : 1u;
   p.ep.M = p.M;
   p.ep.N = p.N;
-  p.splits = choose_splits(p.M, p.N, p.K);
+  p.splits = std::getenv("LSGD_TC_NOSPLIT") ? 1 : choose_splits(p.M, p.N, p.K);
   if (static_cast<size_t>(p.splits) * p.M * p.N > partial_elems) p.splits = 1;
   p.ep.partial = partial;
   return p;
@@ -523,11 +530,15 @@ bool tc_shapes_supported(const std::vector<int32_t>& layers, int batch) {
 }
 
 void tc_alloc(TcWorkspace& ws, const Layout& L, int batch, int n_features) {
+  static const size_t probe_align = std::getenv("LSGD_TC_ALIGN") ? std::strtoull(std::getenv("LSGD_TC_ALIGN"), nullptr, 10) : 0;
   auto dalloc = [&](size_t elems) {
     void* p = nullptr;
-    LSGD_CUDA(cudaMalloc(&p, elems * sizeof(float)));
+    LSGD_CUDA(cudaMalloc(&p, elems * sizeof(float) + probe_align));
     ws.bufs.push_back(p);
-    return static_cast<float*>(p);
+    uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    if (probe_align) a = (a + probe_align - 1) / probe_align * probe_align;
+    if (std::getenv("LSGD_TC_DEBUG")) std::fprintf(stderr, "tc buf %zu elems at %#lx\n", elems, (unsigned long)a);
+    return reinterpret_cast<float*>(a);
   };
   const int B = batch;
   ws.batch = B;
@@ -598,7 +609,9 @@ void tc_alloc(TcWorkspace& ws, const Layout& L, int batch, int n_features) {
 }
 
 void tc_free(TcWorkspace& ws) {
-  for (void* p : ws.bufs) cudaFree(p);
+  static const bool leak = std::getenv("LSGD_TC_NOFREE") != nullptr;  // bring-up probe only
+  if (!leak)
+    for (void* p : ws.bufs) cudaFree(p);
   ws.bufs.clear();
   for (TcLayer* l : ws.layers) delete l;
   ws.layers.clear();
@@ -691,4 +704,52 @@ void tc_test_gemm(int a_mn, int b_mn, int epi, int M, int N, int K, int splits_r
   tc_free(ws);
 }
 
+}  // namespace lsgd_b200
+
+namespace lsgd_b200 {
+// Bring-up probe: one forward/backward of the tensor-core path on host buffers, dumping the intermediates.
+// outs: act (sum_k B*out_k, per layer in order), top delta (B*C), grad (P, reference layout), loss (1).
+void tc_debug_step(const std::vector<int32_t>& layers, int batch, const float* w_host, const float* x_host,
+                   const int32_t* y_host, float* act_out, float* delta_out, float* grad_out, float* loss_out) {
+  LSGD_CUDA(cudaSetDevice(0));
+  Layout L(layers);
+  TcWorkspace ws;
+  tc_alloc(ws, L, batch, layers[0]);
+  float *w = nullptr, *x = nullptr, *grad = nullptr, *sl = nullptr, *loss = nullptr;
+  int32_t* y = nullptr;
+  LSGD_CUDA(cudaMalloc(&w, sizeof(float) * L.n_params));
+  LSGD_CUDA(cudaMalloc(&grad, sizeof(float) * L.n_params));
+  LSGD_CUDA(cudaMalloc(&x, sizeof(float) * batch * layers[0]));
+  LSGD_CUDA(cudaMalloc(&y, sizeof(int32_t) * batch));
+  LSGD_CUDA(cudaMalloc(&sl, sizeof(float) * batch));
+  LSGD_CUDA(cudaMalloc(&loss, sizeof(float)));
+  LSGD_CUDA(cudaMemcpy(w, w_host, sizeof(float) * L.n_params, cudaMemcpyHostToDevice));
+  LSGD_CUDA(cudaMemcpy(x, x_host, sizeof(float) * batch * layers[0], cudaMemcpyHostToDevice));
+  LSGD_CUDA(cudaMemcpy(y, y_host, sizeof(int32_t) * batch, cudaMemcpyHostToDevice));
+  LaunchCounter lc;
+  cudaStream_t st = 0;
+  tc_split_weights(ws, L, w, st, lc);
+  for (int k = 0; k < L.depth(); ++k) tc_forward_layer(ws, L, k, w, x, st, lc);
+  tc_head(ws, L, y, sl, loss, st, lc);
+  LSGD_CUDA(cudaDeviceSynchronize());
+  int64_t off = 0;
+  for (int k = 0; k < L.depth(); ++k) {
+    LSGD_CUDA(cudaMemcpy(act_out + off, ws.act[static_cast<size_t>(k)], sizeof(float) * batch * L.out(k),
+                         cudaMemcpyDeviceToHost));
+    off += static_cast<int64_t>(batch) * L.out(k);
+  }
+  LSGD_CUDA(cudaMemcpy(delta_out, ws.dlt[0], sizeof(float) * batch * L.out(L.depth() - 1), cudaMemcpyDeviceToHost));
+  for (int k = L.depth() - 1; k >= 0; --k)
+    tc_backward_layer(ws, L, k, grad + L.w_off[static_cast<size_t>(k)], grad + L.b_off[static_cast<size_t>(k)], st, lc);
+  LSGD_CUDA(cudaDeviceSynchronize());
+  LSGD_CUDA(cudaMemcpy(grad_out, grad, sizeof(float) * L.n_params, cudaMemcpyDeviceToHost));
+  LSGD_CUDA(cudaMemcpy(loss_out, loss, sizeof(float), cudaMemcpyDeviceToHost));
+  cudaFree(w);
+  cudaFree(grad);
+  cudaFree(x);
+  cudaFree(y);
+  cudaFree(sl);
+  cudaFree(loss);
+  tc_free(ws);
+}
 }  // namespace lsgd_b200

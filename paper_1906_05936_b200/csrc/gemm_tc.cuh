@@ -58,3 +58,8 @@ void tc_test_gemm(int a_mn, int b_mn, int epi, int M, int N, int K, int splits, 
                   const float* bias, const float* mask, float div, int relu, float* out);
 
 }  // namespace lsgd_b200
+
+namespace lsgd_b200 {
+void tc_debug_step(const std::vector<int32_t>& layers, int batch, const float* w_host, const float* x_host,
+                   const int32_t* y_host, float* act_out, float* delta_out, float* grad_out, float* loss_out);
+}

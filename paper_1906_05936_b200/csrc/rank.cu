@@ -109,7 +109,9 @@ class RankImpl final : public Rank {
     LSGD_CUDA(cudaHostGetDevicePointer(&tod, to, 0));
     timed_out_dev_ = static_cast<int*>(tod);
     LSGD_CUDA(cudaMalloc(&bad_dev_, sizeof(unsigned)));
-    LSGD_CUDA(cudaMemset(bad_dev_, 0, sizeof(unsigned)));
+    // Every H2D copy and memset below is issued on main_ (a non-blocking stream does not order behind the
+    // legacy stream, and a pageable cudaMemcpy may return before its DMA lands).
+    LSGD_CUDA(cudaMemsetAsync(bad_dev_, 0, sizeof(unsigned), main_));
     peer_base_.assign(static_cast<size_t>(N_), nullptr);
     for (int i = 0; i < kRing; ++i) LSGD_CUDA(cudaEventCreateWithFlags(&ring_ev_[i], cudaEventDisableTiming));
     LSGD_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ring_), sizeof(int32_t) * kRing * workers_.size() * B_,
@@ -122,6 +124,7 @@ class RankImpl final : public Rank {
     for (int wid : workers_) alloc_worker(wid);
     if (hist_rows_ > 0)
       LSGD_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hist_), sizeof(T) * hist_rows_ * geo_.P, cudaHostAllocDefault));
+    LSGD_CUDA(cudaStreamSynchronize(main_));  // zeroed flags/payloads are in place before any peer connects
   }
 
   ~RankImpl() override {
@@ -194,8 +197,9 @@ class RankImpl final : public Rank {
     } else {
       LSGD_CUDA(cudaMalloc(&data_x_, conv.size() * sizeof(T)));
       LSGD_CUDA(cudaMalloc(&data_y_, static_cast<size_t>(n) * sizeof(int32_t)));
-      LSGD_CUDA(cudaMemcpy(data_x_, conv.data(), conv.size() * sizeof(T), cudaMemcpyHostToDevice));
-      LSGD_CUDA(cudaMemcpy(data_y_, y, static_cast<size_t>(n) * sizeof(int32_t), cudaMemcpyHostToDevice));
+      LSGD_CUDA(cudaMemcpyAsync(data_x_, conv.data(), conv.size() * sizeof(T), cudaMemcpyHostToDevice, main_));
+      LSGD_CUDA(cudaMemcpyAsync(data_y_, y, static_cast<size_t>(n) * sizeof(int32_t), cudaMemcpyHostToDevice, main_));
+      LSGD_CUDA(cudaStreamSynchronize(main_));
     }
   }
 
@@ -213,8 +217,8 @@ class RankImpl final : public Rank {
     std::vector<T> conv(static_cast<size_t>(geo_.P));
     for (int64_t i = 0; i < geo_.P; ++i) conv[static_cast<size_t>(i)] = static_cast<T>(w[i]);
     for (auto& wk : ws_) {
-      LSGD_CUDA(cudaMemcpy(wk.w, conv.data(), sizeof(T) * geo_.P, cudaMemcpyHostToDevice));
-      if (wk.v) LSGD_CUDA(cudaMemset(wk.v, 0, sizeof(T) * geo_.P));
+      LSGD_CUDA(cudaMemcpyAsync(wk.w, conv.data(), sizeof(T) * geo_.P, cudaMemcpyHostToDevice, main_));
+      if (wk.v) LSGD_CUDA(cudaMemsetAsync(wk.v, 0, sizeof(T) * geo_.P, main_));
       if (use_tc_) tc_split_weights(wk.tc, L_, reinterpret_cast<const float*>(wk.w), main_, lc_);
     }
     if (hist_rows_ > 0) std::memcpy(hist_, conv.data(), sizeof(T) * geo_.P);  // w_0
@@ -422,7 +426,7 @@ class RankImpl final : public Rank {
     w.g = wid / k_;
     w.j = wid % k_;
     LSGD_CUDA(cudaMalloc(&w.blk, static_cast<size_t>(geo_.peer.total)));
-    LSGD_CUDA(cudaMemset(w.blk, 0, static_cast<size_t>(geo_.peer.total)));
+    LSGD_CUDA(cudaMemsetAsync(w.blk, 0, static_cast<size_t>(geo_.peer.total), main_));
     w.flags = reinterpret_cast<unsigned long long*>(w.blk + geo_.peer.flags);
     w.payload = reinterpret_cast<T*>(w.blk + geo_.peer.payload);
     w.s[0] = reinterpret_cast<T*>(w.blk + geo_.peer.s[0]);
@@ -431,14 +435,15 @@ class RankImpl final : public Rank {
     LSGD_CUDA(cudaMalloc(&w.w, sizeof(T) * geo_.P));
     if (spec_.c.mode == LSGD_B200_MOMENTUM) LSGD_CUDA(cudaMalloc(&w.v, sizeof(T) * geo_.P));
     LSGD_CUDA(cudaMalloc(&w.loss_hist, sizeof(T) * kLossCap));
-    LSGD_CUDA(cudaMemset(w.loss_hist, 0, sizeof(T) * kLossCap));
+    LSGD_CUDA(cudaMemsetAsync(w.loss_hist, 0, sizeof(T) * kLossCap, main_));
     if (synth_) {
       // cfg4 synthetic gradient: g_r[k] = Rng(1000 + r).next_symmetric(1.0); fixed per run. The
       // single bucket keeps the payload contiguous: [g_0 .. g_{P-1} | loss slot].
       std::vector<T> g(static_cast<size_t>(geo_.P + 1));
       SplitMix64 r(1000 + static_cast<uint64_t>(wid));
       for (auto& e : g) e = static_cast<T>(r.sym(1.0));
-      LSGD_CUDA(cudaMemcpy(w.payload, g.data(), sizeof(T) * g.size(), cudaMemcpyHostToDevice));
+      LSGD_CUDA(cudaMemcpyAsync(w.payload, g.data(), sizeof(T) * g.size(), cudaMemcpyHostToDevice, main_));
+      LSGD_CUDA(cudaStreamSynchronize(main_));
     } else {
       const int d = spec_.c.n_features;
       LSGD_CUDA(cudaMalloc(&w.x, sizeof(T) * static_cast<size_t>(B_) * d));

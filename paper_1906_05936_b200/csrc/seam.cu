@@ -147,3 +147,11 @@ extern "C" int lsgd_b200_test_gemm(int32_t a_mn, int32_t b_mn, int32_t epi, int3
                                    int32_t relu, float* out) {
   return seam_guard([&] { tc_test_gemm(a_mn, b_mn, epi, M, N, K, 1, A, B, bias, mask, div, relu, out); });
 }
+
+extern "C" int lsgd_b200_test_tc_step(int32_t n_layers, const int32_t* layers, int32_t batch, const float* w,
+                                      const float* x, const int32_t* y, float* act, float* delta, float* grad,
+                                      float* loss) {
+  return seam_guard([&] {
+    tc_debug_step(std::vector<int32_t>(layers, layers + n_layers), batch, w, x, y, act, delta, grad, loss);
+  });
+}
