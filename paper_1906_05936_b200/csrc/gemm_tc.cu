@@ -175,21 +175,25 @@ __device__ __forceinline__ void epi_store(const EpiParams& ep, int epi, int row,
   }
 }
 
+// Persistent: grid = min(tiles, SMs); CTA c takes tiles c, c + grid, ... (m fastest, so the CTAs working at the
+// same time share B tiles in L2). Two TMEM accumulators (2 x 256 columns) let the epilogue of tile i overlap the
+// MMAs of tile i+1; the smem stage ring runs continuously across tiles.
 template <bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                        const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo, int epi,
-                       int k_per_split, EpiParams ep) {
+                       int k_per_split, int splits, EpiParams ep) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ alignas(8) uint64_t full_bar[STAGES];
   __shared__ alignas(8) uint64_t empty_bar[STAGES];
-  __shared__ alignas(8) uint64_t acc_bar;
+  __shared__ alignas(8) uint64_t tfull_bar[2];
+  __shared__ alignas(8) uint64_t tempty_bar[2];
   __shared__ uint32_t tmem_slot;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int k0 = blockIdx.z * k_per_split;
+  const int mt = ep.M / BM, nt = ep.N / BN;
+  const int tiles = mt * nt * splits;
   const int nkb = k_per_split / BK;
 
   if (warp == 0 && lane == 0) {
@@ -197,7 +201,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    mbar_init(&acc_bar, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 4);  // one arrival per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (ep.prefetch) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta_hi)) : "memory");
@@ -208,7 +215,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_slot)),
-                 "r"(TMEM_COLS)
+                 "r"(2 * TMEM_COLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -219,76 +226,96 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = static_cast<uint32_t>(kb / STAGES) & 1u;
-        if (kb >= STAGES) mbar_wait(&empty_bar[s], ph ^ 1u);
-        uint8_t* st = smem + s * STAGE_BYTES;
-        mbar_expect_tx(&full_bar[s], STAGE_BYTES);
-        const int k = k0 + kb * BK;
-        load_op<A_MN, BM>(&ta_hi, &full_bar[s], st, m0, k);
-        load_op<A_MN, BM>(&ta_lo, &full_bar[s], st + A_BYTES, m0, k);
-        load_op<B_MN, BN>(&tb_hi, &full_bar[s], st + 2 * A_BYTES, n0, k);
-        load_op<B_MN, BN>(&tb_lo, &full_bar[s], st + 2 * A_BYTES + B_BYTES, n0, k);
+      uint32_t it = 0;  // k-blocks issued by this CTA across all its tiles (stage ring position)
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int z = t / (mt * nt), r = t % (mt * nt);
+        const int m0 = (r % mt) * BM, n0 = (r / mt) * BN, k0 = z * k_per_split;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
+          if (it >= STAGES) mbar_wait(&empty_bar[s], ph ^ 1u);
+          uint8_t* st = smem + s * STAGE_BYTES;
+          mbar_expect_tx(&full_bar[s], STAGE_BYTES);
+          const int k = k0 + kb * BK;
+          load_op<A_MN, BM>(&ta_hi, &full_bar[s], st, m0, k);
+          load_op<A_MN, BM>(&ta_lo, &full_bar[s], st + A_BYTES, m0, k);
+          load_op<B_MN, BN>(&tb_hi, &full_bar[s], st + 2 * A_BYTES, n0, k);
+          load_op<B_MN, BN>(&tb_lo, &full_bar[s], st + 2 * A_BYTES + B_BYTES, n0, k);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_tf32(A_MN, B_MN);
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = static_cast<uint32_t>(kb / STAGES) & 1u;
-        mbar_wait(&full_bar[s], ph);
+      uint32_t it = 0, local = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+        const uint32_t a = local & 1u;
+        if (local >= 2) mbar_wait(&tempty_bar[a], ((local >> 1) & 1u) ^ 1u);  // epilogue drained this slot
         tc_fence_after();
-        const uint32_t st = su32(smem + s * STAGE_BYTES);
-        const uint32_t a_hi = st, a_lo = st + A_BYTES, b_hi = st + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
+        const uint32_t acc_tmem = tmem + a * TMEM_COLS;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          const uint32_t st = su32(smem + s * STAGE_BYTES);
+          const uint32_t a_hi = st, a_lo = st + A_BYTES, b_hi = st + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
-          mma_tf32(tmem, op_desc<A_MN>(a_hi, kk, ep), op_desc<B_MN>(b_lo, kk, ep), idesc, acc);
-          mma_tf32(tmem, op_desc<A_MN>(a_lo, kk, ep), op_desc<B_MN>(b_hi, kk, ep), idesc, 1u);
-          mma_tf32(tmem, op_desc<A_MN>(a_hi, kk, ep), op_desc<B_MN>(b_hi, kk, ep), idesc, 1u);
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t accum = (kb > 0 || kk > 0) ? 1u : 0u;
+            mma_tf32(acc_tmem, op_desc<A_MN>(a_hi, kk, ep), op_desc<B_MN>(b_lo, kk, ep), idesc, accum);
+            mma_tf32(acc_tmem, op_desc<A_MN>(a_lo, kk, ep), op_desc<B_MN>(b_hi, kk, ep), idesc, 1u);
+            mma_tf32(acc_tmem, op_desc<A_MN>(a_hi, kk, ep), op_desc<B_MN>(b_hi, kk, ep), idesc, 1u);
+          }
+          mma_commit(&empty_bar[s]);  // stage s is free once these MMAs have read it
         }
-        mma_commit(&empty_bar[s]);  // stage s is free once these MMAs have read it
+        mma_commit(&tfull_bar[a]);  // accumulator slot a holds the finished tile
       }
-      mma_commit(&acc_bar);
     }
   } else {
     // epilogue warps 2..5 -> TMEM lane quadrant warp % 4
-    mbar_wait(&acc_bar, 0);
-    tc_fence_after();
     const int q = warp & 3;
-    const int row = m0 + q * 32 + lane;
-    EpiParams e = ep;
-    int mode = epi;
-    if (gridDim.z > 1) {
-      mode = kRaw;
-      e.partial = ep.partial + static_cast<int64_t>(blockIdx.z) * ep.M * ep.N;
-    }
+    uint32_t local = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+      const int z = t / (mt * nt), r = t % (mt * nt);
+      const int m0 = (r % mt) * BM, n0 = (r / mt) * BN;
+      const uint32_t a = local & 1u;
+      mbar_wait(&tfull_bar[a], (local >> 1) & 1u);
+      tc_fence_after();
+      const int row = m0 + q * 32 + lane;
+      EpiParams e = ep;
+      int mode = epi;
+      if (splits > 1) {
+        mode = kRaw;
+        e.partial = ep.partial + static_cast<int64_t>(z) * ep.M * ep.N;
+      }
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t r[32];
-      const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
-          "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-            "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-            "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      float v[32];
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t rr[32];
+        const uint32_t taddr = tmem + a * TMEM_COLS + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+            "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(rr[0]), "=r"(rr[1]), "=r"(rr[2]), "=r"(rr[3]), "=r"(rr[4]), "=r"(rr[5]), "=r"(rr[6]), "=r"(rr[7]),
+              "=r"(rr[8]), "=r"(rr[9]), "=r"(rr[10]), "=r"(rr[11]), "=r"(rr[12]), "=r"(rr[13]), "=r"(rr[14]),
+              "=r"(rr[15]), "=r"(rr[16]), "=r"(rr[17]), "=r"(rr[18]), "=r"(rr[19]), "=r"(rr[20]), "=r"(rr[21]),
+              "=r"(rr[22]), "=r"(rr[23]), "=r"(rr[24]), "=r"(rr[25]), "=r"(rr[26]), "=r"(rr[27]), "=r"(rr[28]),
+              "=r"(rr[29]), "=r"(rr[30]), "=r"(rr[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        float v[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-      epi_store(e, mode, row, n0 + c, v);
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(rr[i]);
+        epi_store(e, mode, row, n0 + c, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty_bar[a])) : "memory");
     }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TMEM_COLS) : "memory");
   }
 }
 
@@ -449,9 +476,15 @@ void launch_variant(const GemmPlan& p, cudaStream_t st) {
       configured |= 1ull << dev;
     }
   }
-  dim3 grid(p.N / BN, p.M / BM, p.splits);
+  static int sms = [] {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, 0);
+    return v > 0 ? v : 148;
+  }();
+  const int tiles = (p.N / BN) * (p.M / BM) * p.splits;
+  const int grid = tiles < sms ? tiles : sms;
   gemm_tf32x3_kernel<A_MN, B_MN><<<grid, THREADS, SMEM_BYTES, st>>>(p.a_hi, p.a_lo, p.b_hi, p.b_lo, p.epi,
-                                                                    p.K / p.splits, p.ep);
+                                                                    p.K / p.splits, p.splits, p.ep);
 }
 
 void run_plan(const GemmPlan& p, cudaStream_t st, LaunchCounter& lc) {
