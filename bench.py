@@ -231,7 +231,7 @@ def run_b200_arm(args):
     launches = r.launches() - l0
     clk = clocks.finish() if clocks else None
     r.timing(False)
-    fams = {f: r.kernel_time(f) for f in ("gemm", "reduce", "global", "update", "gather")}
+    fams = {f: r.kernel_time(f) for f in ("gemm", "reduce", "global", "broadcast", "update", "gather")}
     ms_all = allgather(ms)
     ms_max = max(ms_all)
     B = cfg.local_batch

@@ -18,6 +18,10 @@ extern "C" {
 int lsgd_b200_test_gemm(int32_t a_mn, int32_t b_mn, int32_t epi, int32_t M, int32_t N, int32_t K, const float* A,
                         const float* B, const float* bias, const float* mask, float div, int32_t relu, float* out);
 
+/* Device time (CUDA events, average over reps launches) of the tensor-core GEMM of that shape and majors. */
+int lsgd_b200_test_gemm_timed(int32_t a_mn, int32_t b_mn, int32_t epi, int32_t M, int32_t N, int32_t K, int32_t reps,
+                              double* avg_ms);
+
 /* One forward + backward of the tensor-core path on host buffers (w [P], x [batch*layers[0]] fp32, y [batch]),
  * returning the activations of every layer (concatenated), the top delta, the gradient [P] and the mean loss. */
 int lsgd_b200_test_tc_step(int32_t n_layers, const int32_t* layers, int32_t batch, const float* w, const float* x,

@@ -28,10 +28,13 @@ struct PeerLayout {
   int64_t payload = 0;   // Ppad elements
   int64_t s[2] = {0, 0};  // Sg elements each (double-buffered by step parity)
   int64_t gbar = 0;      // Sg elements
+  int64_t gfull = 0;     // Ppad elements: the whole averaged gradient, pushed here by the group's slot owners
   int64_t total = 0;
 };
 enum : int { kFlagGrad = 0, kFlagSlice = 1, kFlagBcast = 2 };
 constexpr int kMaxBuckets = 32;
+// flags[kArrived + b * kMaxPeers + j]: round counter of the averaged sub-slice j of bucket b pushed by slot j
+constexpr int kArrived = 3 * kMaxBuckets;
 
 // Gradient buckets: one per layer (that layer's [W_k | b_k] block, contiguous in the reference's parameter
 // layout, mlp.hpp:14-18), the loss slot riding the last layer's bucket. Each bucket is split into k sub-slices of

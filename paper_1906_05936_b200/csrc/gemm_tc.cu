@@ -11,6 +11,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -22,7 +23,9 @@ namespace lsgd_b200 {
 
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 32, STAGES = 2, THREADS = 192;
+// BK = 16: 48 KB stages, 4 deep (the producer keeps 3 K blocks in flight ahead of the MMAs).
+constexpr int BM = 128, BN = 256, BK = 16, STAGES = 4, THREADS = 192;
+constexpr int MN_CHUNK_BYTES = BK * 128;  // one 32-wide MN chunk of an MN-major tile: BK rows of 128 B
 constexpr int A_BYTES = BM * BK * 4;                        // 16 KB
 constexpr int B_BYTES = BN * BK * 4;                        // 32 KB
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;      // 96 KB
@@ -45,6 +48,8 @@ struct EpiParams {
   int M, N;
   uint32_t mn_lbo, mn_sbo, mn_layout;  // MN-major descriptor geometry (see op_desc)
   uint32_t prefetch;                   // prefetch.tensormap the four operand maps
+  int div_pow2;                        // div is a power of two: multiply by the exact reciprocal
+  float div_inv;
 };
 
 // ------------------------------------------------------------------------------------------ PTX helpers
@@ -114,10 +119,11 @@ __host__ __device__ constexpr uint32_t idesc_tf32(bool a_mn, bool b_mn) {
 // Descriptor of operand tile `base` (R rows/cols of MN, 32 K) for the kk-th 8-wide K step.
 template <bool MN>
 __device__ __forceinline__ uint64_t op_desc(uint32_t base, int kk, const EpiParams& ep) {
-  // MN-major: 32-col MN chunks 4 KB apart (LBO), 4-row K atoms 512 B apart (SBO), +8 K rows = +1 KB per K step
+  // MN-major: 32-col MN chunks BK*128 B apart (LBO), 4-row K atoms 512 B apart (SBO), +8 K rows = +1 KB per K step
   if (MN) return sdesc(base + kk * 1024, ep.mn_lbo, ep.mn_sbo, ep.mn_layout);
-  // K-major: 128 B K rows, 8-row groups 1 KB apart (SBO), +32 B per 8-wide K step inside the swizzle atom
-  return sdesc(base + kk * 32, 16, 1024, 2);
+  // K-major: one 64 B row of BK = 16 tf32 per M/N row (written by TMA SWIZZLE_64B)
+  static_assert(BK == 16, "K-major descriptors assume 64 B rows (SWIZZLE_64B)");
+  return sdesc(base + kk * 32, 16, 512, 4);  // SWIZZLE_64B: 64 B K rows, 8-row atoms 512 B apart, +32 B per K step
 }
 
 // TMA of one operand tile (R along M/N) for K block starting at k.
@@ -125,7 +131,7 @@ template <bool MN, int R>
 __device__ __forceinline__ void load_op(const CUtensorMap* map, uint64_t* bar, uint8_t* dst, int r0, int k) {
   if (MN) {
 #pragma unroll
-    for (int c = 0; c < R / 32; ++c) tma_2d(map, bar, dst + c * 4096, r0 + 32 * c, k);
+    for (int c = 0; c < R / 32; ++c) tma_2d(map, bar, dst + c * MN_CHUNK_BYTES, r0 + 32 * c, k);
   } else {
     tma_2d(map, bar, dst, k, r0);
   }
@@ -153,7 +159,7 @@ __device__ __forceinline__ void epi_store(const EpiParams& ep, int epi, int row,
       v = __fadd_rn(v, __ldg(ep.bias + col0 + i));
       if (ep.relu && v < 0.f) v = 0.f;
     } else if (epi == kWgrad) {
-      v = __fdiv_rn(v, ep.div);
+      v = ep.div_pow2 ? v * ep.div_inv : __fdiv_rn(v, ep.div);  // x * 2^-k is exactly x / 2^k
     } else {
       if (!(__ldg(ep.mask + static_cast<int64_t>(row) * ep.ldm + col0 + i) > 0.f)) v = 0.f;
     }
@@ -363,29 +369,52 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, int64_t n, float*
   }
 }
 
-// Softmax-CE head for the tensor-core path: one thread per sample (same arithmetic as kernels.cu's head), also
-// writing the hi/lo split of delta for the backward GEMMs.
+// Softmax-CE head for the tensor-core path: one warp per sample, lanes striding the classes (coalesced), max and
+// sum by warp shuffles; writes delta = softmax - onehot and its hi/lo split for the backward GEMMs.
 __global__ void softmax_xent_split_kernel(const float* __restrict__ logits, const int32_t* __restrict__ labels, int b,
                                           int c, float* __restrict__ delta, float* __restrict__ dhi,
                                           float* __restrict__ dlo, float* __restrict__ sample_loss) {
-  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  const int s = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
   if (s >= b) return;
   const float* z = logits + static_cast<int64_t>(s) * c;
-  float zmax = z[0];
-  for (int k = 1; k < c; ++k) zmax = (zmax < z[k]) ? z[k] : zmax;
+  float zmax = -INFINITY;
+  for (int k = lane; k < c; k += 32) zmax = fmaxf(zmax, z[k]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) zmax = fmaxf(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
   float sum = 0.f;
-  for (int k = 0; k < c; ++k) sum = __fadd_rn(sum, expf(__fsub_rn(z[k], zmax)));
-  const float lse = __fadd_rn(zmax, logf(sum));
+  for (int k = lane; k < c; k += 32) sum += expf(z[k] - zmax);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float lse = zmax + logf(sum);
   const int lab = labels[s];
-  sample_loss[s] = __fsub_rn(lse, z[lab]);
-  for (int k = 0; k < c; ++k) {
-    float p = expf(__fsub_rn(z[k], lse));
-    float d = (k == lab) ? __fsub_rn(p, 1.f) : p;
+  if (lane == 0) sample_loss[s] = lse - z[lab];
+  for (int k = lane; k < c; k += 32) {
+    const float p = expf(z[k] - lse);
+    const float d = (k == lab) ? p - 1.f : p;
     const int64_t at = static_cast<int64_t>(s) * c + k;
     delta[at] = d;
-    float h = tf32_rna(d);
+    const float h = tf32_rna(d);
     dhi[at] = h;
     dlo[at] = tf32_rna(d - h);
+  }
+}
+
+// Bias gradient for the fp32 path: db[j] = (sum_s delta[s, j]) / B. 32 columns x 8 row-partitions per block,
+// partials combined in a fixed order (deterministic, no atomics).
+__global__ void bias_grad_f32_kernel(const float* __restrict__ delta, int b, int n, float* __restrict__ db) {
+  __shared__ float part[8][33];
+  const int j = blockIdx.x * 32 + threadIdx.x;
+  float acc = 0.f;
+  if (j < n)
+    for (int r = threadIdx.y; r < b; r += 8) acc += delta[static_cast<int64_t>(r) * n + j];
+  part[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && j < n) {
+    float t = part[0][threadIdx.x];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) t += part[q][threadIdx.x];
+    db[j] = __fdiv_rn(t, static_cast<float>(b));
   }
 }
 
@@ -408,7 +437,7 @@ EncodeFn encode_fn() {
 // MN-major operand geometry: TMA swizzle SWIZZLE_128B_ATOM_32B + UMMA layout SWIZZLE_128B_BASE32B, LBO = MN chunk
 // stride, SBO = 4-row K atom stride. LSGD_TC_MN="lbo,sbo,layout,tma_swizzle" overrides it (bring-up only).
 struct MnGeometry {
-  uint32_t lbo = 4096, sbo = 512, layout = 1, tma_swizzle = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+  uint32_t lbo = MN_CHUNK_BYTES, sbo = 512, layout = 1, tma_swizzle = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
 };
 const MnGeometry& mn_geometry() {
   static MnGeometry g = [] {
@@ -448,7 +477,7 @@ CUtensorMap make_map(const OpView& v, int tile_rows) {
   strides[0] = static_cast<cuuint64_t>(v.ld) * 4;
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(v.ptr), dims, strides, box, estr,
                            CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           v.mn ? static_cast<CUtensorMapSwizzle>(mn_geometry().tma_swizzle) : CU_TENSOR_MAP_SWIZZLE_128B,
+                           v.mn ? static_cast<CUtensorMapSwizzle>(mn_geometry().tma_swizzle) : CU_TENSOR_MAP_SWIZZLE_64B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   check<Error>(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (", static_cast<int>(r), ")");
   return m;
@@ -539,6 +568,9 @@ GemmPlan make_plan(const OpView& a_hi, const float* a_lo, const OpView& b_hi, co
   p.ep.mn_layout = g.layout;
   static const bool no_prefetch = std::getenv("LSGD_TC_NOPREFETCH") != nullptr;  // bring-up probe only
   p.ep.prefetch = no_prefetch ? 0u : 1u;
+  int ex = 0;
+  p.ep.div_pow2 = (ep.div > 0.f && std::frexp(ep.div, &ex) == 0.5f) ? 1 : 0;
+  p.ep.div_inv = p.ep.div_pow2 ? 1.0f / ep.div : 0.f;
   p.ep.M = p.M;
   p.ep.N = p.N;
   p.splits = std::getenv("LSGD_TC_NOSPLIT") ? 1 : choose_splits(p.M, p.N, p.K);
@@ -678,7 +710,7 @@ void tc_head(TcWorkspace& ws, const Layout& L, const int32_t* y, float* sample_l
   const int B = ws.batch;
   const int C = L.out(depth - 1);
   const int top = 0;  // delta of layer depth-1 lives in ping-pong slot (depth-1-(depth-1)) & 1 = 0
-  softmax_xent_split_kernel<<<(B + 127) / 128, 128, 0, st>>>(ws.act[static_cast<size_t>(depth - 1)], y, B, C,
+  softmax_xent_split_kernel<<<(B + 7) / 8, 256, 0, st>>>(ws.act[static_cast<size_t>(depth - 1)], y, B, C,
                                                              ws.dlt[top], ws.dlt_hi[top], ws.dlt_lo[top], sample_loss);
   ++lc.n;
   LSGD_CUDA(cudaGetLastError());
@@ -692,13 +724,14 @@ void tc_backward_layer(TcWorkspace& ws, const Layout& L, int k, float* gW, float
   GemmPlan pw = tl->wgrad;
   pw.ep.out = gW;
   run_plan(pw, st, lc);
-  launch_bias_grad<float>(ws.dlt[di], ws.batch, L.out(k), gb, st, lc);
+  bias_grad_f32_kernel<<<(L.out(k) + 31) / 32, dim3(32, 8), 0, st>>>(ws.dlt[di], ws.batch, L.out(k), gb);
+  ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
   if (tl->has_igrad) run_plan(tl->igrad, st, lc);
 }
 
-void tc_test_gemm(int a_mn, int b_mn, int epi, int M, int N, int K, int splits_req, const float* A, const float* Bm,
-                  const float* bias, const float* mask, float div, int relu, float* out) {
-  (void)splits_req;
+void tc_test_gemm(int a_mn, int b_mn, int epi, int M, int N, int K, int reps, const float* A, const float* Bm,
+                  const float* bias, const float* mask, float div, int relu, float* out, double* avg_ms) {
   LSGD_CUDA(cudaSetDevice(0));
   TcWorkspace ws;
   auto dalloc = [&](size_t elems) {
@@ -732,6 +765,20 @@ void tc_test_gemm(int a_mn, int b_mn, int epi, int M, int N, int K, int splits_r
   OpView va{ah, M, K, a_mn ? M : K, a_mn != 0}, vb{bh, N, K, b_mn ? N : K, b_mn != 0};
   GemmPlan p = make_plan(va, al, vb, bl, epi, ep, part, pe);
   run_plan(p, 0, lc);
+  if (reps > 1 && avg_ms) {  // device-timed repetitions (bring-up / tuning)
+    cudaEvent_t e0, e1;
+    LSGD_CUDA(cudaEventCreate(&e0));
+    LSGD_CUDA(cudaEventCreate(&e1));
+    LSGD_CUDA(cudaEventRecord(e0, 0));
+    for (int r = 0; r < reps; ++r) run_plan(p, 0, lc);
+    LSGD_CUDA(cudaEventRecord(e1, 0));
+    LSGD_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    LSGD_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *avg_ms = ms / reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
   LSGD_CUDA(cudaDeviceSynchronize());
   LSGD_CUDA(cudaMemcpy(out, o, no * 4, cudaMemcpyDeviceToHost));
   tc_free(ws);

@@ -54,8 +54,8 @@ void tc_backward_layer(TcWorkspace& ws, const Layout& L, int k, float* gW, float
 // Standalone GEMM for conformance tests: D = A * B^T with A [M x K], B [N x K] given in their storage major
 // (K-major: [rows][K]; MN-major: [K][rows]), epilogue 0 forward (bias, relu), 1 weight-grad (/div), 2 input-grad
 // (mask). Host buffers.
-void tc_test_gemm(int a_mn, int b_mn, int epi, int M, int N, int K, int splits, const float* A, const float* B,
-                  const float* bias, const float* mask, float div, int relu, float* out);
+void tc_test_gemm(int a_mn, int b_mn, int epi, int M, int N, int K, int reps, const float* A, const float* B,
+                  const float* bias, const float* mask, float div, int relu, float* out, double* avg_ms = nullptr);
 
 }  // namespace lsgd_b200
 

@@ -366,6 +366,24 @@ __global__ void wait_flags_kernel(FlagList fl, int n, unsigned long long target,
   __syncthreads();
 }
 
+template <typename T>
+__global__ void __launch_bounds__(256) push_kernel(const T* __restrict__ src, int64_t len, DstList<T> dst, int n_dst) {
+  constexpr int V = Vec<T>::kN;
+  const int64_t nvec = len / V;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nvec; i += stride) {
+    const Vec<T> v = ld16(src + i * V);
+    for (int d = 0; d < n_dst; ++d) st16(dst.p[d] + i * V, v);
+  }
+  for (int64_t e = nvec * V + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < len; e += stride)
+    for (int d = 0; d < n_dst; ++d) dst.p[d][e] = src[e];
+}
+
+__global__ void signal_many_kernel(SignalList fl, int n, unsigned long long v) {
+  __threadfence_system();
+  if (threadIdx.x < n) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(fl.f[threadIdx.x]), "l"(v) : "memory");
+}
+
 __global__ void signal_flag_kernel(unsigned long long* f, unsigned long long v) {
   __threadfence_system();
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(v) : "memory");
@@ -484,6 +502,19 @@ void launch_signal_flag(unsigned long long* flag, unsigned long long value, cuda
   LSGD_CUDA(cudaGetLastError());
 }
 
+template <typename T>
+void launch_push(const T* src, int64_t len, DstList<T> dst, int n_dst, cudaStream_t st, LaunchCounter& lc) {
+  push_kernel<T><<<grid_for(len / Vec<T>::kN + 1, 256, 148 * 2), 256, 0, st>>>(src, len, dst, n_dst);
+  ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
+}
+
+void launch_signal_many(SignalList flags, int n, unsigned long long value, cudaStream_t st, LaunchCounter& lc) {
+  signal_many_kernel<<<1, 32, 0, st>>>(flags, n, value);
+  ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
+}
+
 void launch_sleep(double seconds, cudaStream_t st, LaunchCounter& lc) {
   if (seconds <= 0.0) return;
   sleep_kernel<<<1, 1, 0, st>>>(static_cast<unsigned long long>(seconds * 1e9));
@@ -515,7 +546,8 @@ void launch_to_f64(const T* src, int64_t n, double* dst, cudaStream_t st, Launch
   template void launch_ordered_sum<T>(SrcList<T>, int, int64_t, T*, bool, T, cudaStream_t, LaunchCounter&);        \
   template void launch_update<T>(const UpdateArgs<T>&, bool, cudaStream_t, LaunchCounter&);                        \
   template void launch_from_f64<T>(const double*, int64_t, T*, cudaStream_t, LaunchCounter&);                      \
-  template void launch_to_f64<T>(const T*, int64_t, double*, cudaStream_t, LaunchCounter&);
+  template void launch_to_f64<T>(const T*, int64_t, double*, cudaStream_t, LaunchCounter&);                       \
+  template void launch_push<T>(const T*, int64_t, DstList<T>, int, cudaStream_t, LaunchCounter&);
 
 LSGD_INSTANTIATE(float)
 LSGD_INSTANTIATE(double)

@@ -76,7 +76,21 @@ struct UpdateArgs {
 template <typename T>
 void launch_update(const UpdateArgs<T>& a, bool exact, cudaStream_t st, LaunchCounter& lc);
 
+// --- broadcast as a push: copy an averaged slice into n destinations (the group members' full-gradient
+// buffers, k-1 of them over NVLink) so the update kernel reads local HBM only.
+template <typename T>
+struct DstList {
+  T* p[kMaxPeers];
+};
+template <typename T>
+void launch_push(const T* src, int64_t len, DstList<T> dst, int n_dst, cudaStream_t st, LaunchCounter& lc);
+
 // --- cross-GPU flags: monotone step counters in peer memory -------------------------------------------------
+struct SignalList {
+  unsigned long long* f[kMaxPeers];
+};
+// System-scope release store of `value` into n (possibly remote) flags after all prior work of the stream.
+void launch_signal_many(SignalList flags, int n, unsigned long long value, cudaStream_t st, LaunchCounter& lc);
 struct FlagList {
   const volatile unsigned long long* f[kMaxPeers];
 };

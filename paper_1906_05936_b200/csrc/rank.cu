@@ -66,11 +66,12 @@ Geometry::Geometry(const RunSpec& spec, int es) : esize(es) {
   Sg = goff;
   loss_at = buckets.back().poff + buckets.back().n;
   peer.flags = 0;
-  peer.payload = round_up(3 * kMaxBuckets * 8, 256);
+  peer.payload = round_up((kArrived + kMaxBuckets * kMaxPeers) * 8, 256);
   peer.s[0] = round_up(peer.payload + Ppad * es, 256);
   peer.s[1] = round_up(peer.s[0] + Sg * es, 256);
   peer.gbar = round_up(peer.s[1] + Sg * es, 256);
-  peer.total = round_up(peer.gbar + Sg * es, 256);
+  peer.gfull = round_up(peer.gbar + Sg * es, 256);
+  peer.total = round_up(peer.gfull + Ppad * es, 256);
 }
 
 // ================================================================================================ RankImpl
@@ -100,6 +101,9 @@ class RankImpl final : public Rank {
     split_ = workers_.size() == 1;
     if (split_) LSGD_CUDA(cudaStreamCreateWithPriority(&comm_, cudaStreamNonBlocking, hi));
     else comm_ = main_;
+    if (split_) LSGD_CUDA(cudaStreamCreateWithFlags(&upd_, cudaStreamNonBlocking));
+    else upd_ = main_;
+    for (int b = 0; b < kMaxBuckets; ++b) LSGD_CUDA(cudaEventCreateWithFlags(&ev_upd_[b], cudaEventDisableTiming));
     for (int b = 0; b < kMaxBuckets; ++b) LSGD_CUDA(cudaEventCreateWithFlags(&ev_bucket_[b], cudaEventDisableTiming));
     void* to = nullptr;
     LSGD_CUDA(cudaHostAlloc(&to, sizeof(int), cudaHostAllocMapped));
@@ -159,7 +163,11 @@ class RankImpl final : public Rank {
     cudaFree(bad_dev_);
     for (int i = 0; i < kRing; ++i) cudaEventDestroy(ring_ev_[i]);
     for (int b = 0; b < kMaxBuckets; ++b) cudaEventDestroy(ev_bucket_[b]);
-    if (split_) cudaStreamDestroy(comm_);
+    if (split_) {
+      cudaStreamDestroy(comm_);
+      cudaStreamDestroy(upd_);
+    }
+    for (int b = 0; b < kMaxBuckets; ++b) cudaEventDestroy(ev_upd_[b]);
     cudaStreamDestroy(main_);
   }
 
@@ -265,8 +273,8 @@ class RankImpl final : public Rank {
     if (alg_ == LSGD_B200_LSGD && applied_ < t_next_) {
       current_phase() = "broadcast";
       for (auto& wk : ws_)
-        for (int b = 0; b < nb_; ++b) apply_bucket(wk, b, t_next_ - 1);
-      for (auto& wk : ws_) after_update(wk, t_next_ - 1);
+        for (int b = 0; b < nb_; ++b) apply_bucket(wk, b, t_next_ - 1, main_);
+      for (auto& wk : ws_) after_update(wk, t_next_ - 1, main_);
       ++applied_;
     }
     synchronize();
@@ -275,6 +283,7 @@ class RankImpl final : public Rank {
   void synchronize() override {
     LSGD_CUDA(cudaSetDevice(dev_));
     LSGD_CUDA(cudaStreamSynchronize(comm_));
+    LSGD_CUDA(cudaStreamSynchronize(upd_));
     LSGD_CUDA(cudaStreamSynchronize(main_));
     check_health();
     unsigned bad = 0;
@@ -401,6 +410,7 @@ class RankImpl final : public Rank {
     T* payload = nullptr;
     T* s[2] = {nullptr, nullptr};
     T* gbar = nullptr;
+    T* gfull = nullptr;
     T* w = nullptr;
     T* v = nullptr;
     T* x = nullptr;
@@ -432,6 +442,7 @@ class RankImpl final : public Rank {
     w.s[0] = reinterpret_cast<T*>(w.blk + geo_.peer.s[0]);
     w.s[1] = reinterpret_cast<T*>(w.blk + geo_.peer.s[1]);
     w.gbar = reinterpret_cast<T*>(w.blk + geo_.peer.gbar);
+    w.gfull = reinterpret_cast<T*>(w.blk + geo_.peer.gfull);
     LSGD_CUDA(cudaMalloc(&w.w, sizeof(T) * geo_.P));
     if (spec_.c.mode == LSGD_B200_MOMENTUM) LSGD_CUDA(cudaMalloc(&w.v, sizeof(T) * geo_.P));
     LSGD_CUDA(cudaMalloc(&w.loss_hist, sizeof(T) * kLossCap));
@@ -491,6 +502,29 @@ class RankImpl final : public Rank {
   T* peer_payload(int wid) const { return reinterpret_cast<T*>(base(wid) + geo_.peer.payload); }
   T* peer_s(int wid, int par) const { return reinterpret_cast<T*>(base(wid) + geo_.peer.s[par]); }
   T* peer_gbar(int wid) const { return reinterpret_cast<T*>(base(wid) + geo_.peer.gbar); }
+  T* peer_gfull(int wid) const { return reinterpret_cast<T*>(base(wid) + geo_.peer.gfull); }
+  unsigned long long* peer_arrived(int wid, int b, int j) const {
+    return reinterpret_cast<unsigned long long*>(base(wid) + geo_.peer.flags) + kArrived + b * kMaxPeers + j;
+  }
+
+  // Broadcast of bucket b's averaged sub-slice j (executors.cpp:297-299) as a push into every group member's gfull
+  // (k-1 of them over NVLink), then a release of the member's arrival flag; runs on the comm stream, off the
+  // update's critical path.
+  void push_bucket(Worker& w, int b, int64_t t, cudaStream_t st) {
+    const Bucket& bk = geo_.buckets[static_cast<size_t>(b)];
+    auto members = group_members(w.g);
+    DstList<T> dst{};
+    SignalList sl{};
+    for (int i = 0; i < k_; ++i) {
+      dst.p[i] = peer_gfull(members[static_cast<size_t>(i)]) + bk.poff + w.j * bk.S;
+      sl.f[i] = peer_arrived(members[static_cast<size_t>(i)], b, w.j);
+    }
+    {
+      Timed tm(this, "broadcast", st);
+      launch_push<T>(w.gbar + bk.goff, bk.S, dst, k_, st, lc_);
+    }
+    launch_signal_many(sl, k_, static_cast<unsigned long long>(t + 1), st, lc_);
+  }
   const volatile unsigned long long* peer_flag(int wid, int which, int b) const {
     return reinterpret_cast<const volatile unsigned long long*>(base(wid) + geo_.peer.flags) + which * kMaxBuckets + b;
   }
@@ -675,7 +709,7 @@ class RankImpl final : public Rank {
       Timed tm(this, "reduce", st);
       launch_ordered_sum<T>(src, k_, bk.S, dst, alg_ == LSGD_B200_LSGD, static_cast<T>(N_), st, lc_);
     }
-    if (G_ == 1) signal(w, kFlagBcast, b, static_cast<unsigned long long>(t + 1), st);
+    if (G_ == 1) push_bucket(w, b, t, st);
     else if (slice_comm_ == nullptr) signal(w, kFlagSlice, b, static_cast<unsigned long long>(t + 1), st);
   }
 
@@ -698,15 +732,15 @@ class RankImpl final : public Rank {
       Timed tm(this, "global", st);
       launch_ordered_sum<T>(src, G_, bk.S, w.gbar + bk.goff, false, T(0), st, lc_);
     }
-    signal(w, kFlagBcast, b, static_cast<unsigned long long>(t + 1), st);
+    push_bucket(w, b, t, st);
   }
 
   // K8 for bucket b of round u (executors.cpp:210-229): pull the k averaged sub-slices of the group, apply
   // sgd_update to the bucket's parameters, check finiteness, record the loss (last bucket).
-  void apply_bucket(Worker& w, int b, int64_t u) {
+  void apply_bucket(Worker& w, int b, int64_t u, cudaStream_t st) {
     const Bucket& bk = geo_.buckets[static_cast<size_t>(b)];
     const size_t wi = widx(w);
-    if (b == 0) phase_mark(wi, u, 4, 0, main_);
+    if (b == 0) phase_mark(wi, u, 4, 0, st);
     UpdateArgs<T> a{};
     a.slice_len = bk.S;
     a.n_params = bk.n;
@@ -718,13 +752,15 @@ class RankImpl final : public Rank {
       }
       if (flat_nccl()) a.post_div = static_cast<T>(N_);  // the per-worker /N after the flat allreduce (:170)
     } else {
-      auto owners = group_members(w.g);
-      wait(owners, kFlagBcast, b, static_cast<unsigned long long>(u + 1), main_);
-      for (int j = 0; j < k_; ++j) a.slices.p[j] = peer_gbar(owners[static_cast<size_t>(j)]) + bk.goff;
+      FlagList fl{};  // the k sub-slices of round u have been pushed into this worker's gfull
+      for (int j = 0; j < k_; ++j) fl.f[j] = peer_arrived(w.id, b, j);
+      launch_wait_flags(fl, k_, static_cast<unsigned long long>(u + 1), timeout_ns(), timed_out_dev_, st, lc_);
+      a.slices.p[0] = w.gfull + bk.poff;
+      a.slice_len = bk.S * k_;
     }
     if (b == 0) {
-      phase_mark(wi, u, 4, 1, main_);
-      phase_mark(wi, u, 5, 0, main_);
+      phase_mark(wi, u, 4, 1, st);
+      phase_mark(wi, u, 5, 0, st);
     }
     a.w = w.w + bk.pstart;
     a.v = w.v ? w.v + bk.pstart : nullptr;
@@ -738,14 +774,14 @@ class RankImpl final : public Rank {
       a.w_hi = w.tc.w_hi + bk.pstart;
       a.w_lo = w.tc.w_lo + bk.pstart;
     }
-    Timed tm(this, "update", main_);
-    launch_update<T>(a, exact_, main_, lc_);
+    Timed tm(this, "update", st);
+    launch_update<T>(a, exact_, st, lc_);
   }
 
-  void after_update(Worker& w, int64_t u) {
-    phase_mark(widx(w), u, 5, 1, main_);
+  void after_update(Worker& w, int64_t u, cudaStream_t st) {
+    phase_mark(widx(w), u, 5, 1, st);
     if (hist_rows_ > 0 && w.id == workers_[0] && u + 1 < hist_rows_)
-      LSGD_CUDA(cudaMemcpyAsync(hist_ + (u + 1) * geo_.P, w.w, sizeof(T) * geo_.P, cudaMemcpyDeviceToHost, main_));
+      LSGD_CUDA(cudaMemcpyAsync(hist_ + (u + 1) * geo_.P, w.w, sizeof(T) * geo_.P, cudaMemcpyDeviceToHost, st));
   }
 
   // ------------------------------------------------------------------------------------------ one step
@@ -755,27 +791,40 @@ class RankImpl final : public Rank {
     if (!synth_) io(t, given, shard_only);
     else launch_sleep(spec_.c.io_delay_s, main_, lc_);
 
-    // postponed update of round t-1, bucket by bucket, each right before the forward of its layer
+    // postponed update of round t-1, bucket by bucket, each finished right before the forward of its layer.
+    // One worker per rank: the updates run on their own stream, so bucket k+1's update (waiting for its averaged
+    // gradient, then streaming w/v through HBM) overlaps the forward GEMM of layer k.
     const bool postponed = alg_ == LSGD_B200_LSGD && t >= 1;
+    if (postponed && split_) {
+      Worker& w = ws_[0];
+      current_phase() = "broadcast";
+      for (int k = 0; k < D; ++k) {
+        if (reduce_folded()) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_bucket_[k], 0));  // payload k of round t-1
+        apply_bucket(w, k, t - 1, upd_);
+        LSGD_CUDA(cudaEventRecord(ev_upd_[k], upd_));
+      }
+      after_update(w, t - 1, upd_);
+    }
     for (auto& w : ws_) {
       current_phase() = "compute";
       phase_mark(widx(w), t, 1, 0, main_);
       for (int k = 0; k < D; ++k) {
-        if (postponed) {
+        if (postponed && split_) {
+          LSGD_CUDA(cudaStreamWaitEvent(main_, ev_upd_[k], 0));
+        } else if (postponed) {
           current_phase() = "broadcast";
-          apply_bucket(w, k, t - 1);
+          apply_bucket(w, k, t - 1, main_);
           current_phase() = "compute";
         }
         forward_layer(w, k);
       }
-      if (postponed) after_update(w, t - 1);
+      if (postponed && !split_) after_update(w, t - 1, main_);
       head(w);
       for (int k = D - 1; k >= 0; --k) {
         backward_layer(w, k);
-        if (!flat_nccl() && !reduce_folded() && alg_ != LSGD_B200_SEQUENTIAL) {
+        if (!flat_nccl() && !reduce_folded() && alg_ != LSGD_B200_SEQUENTIAL)
           signal(w, kFlagGrad, k, static_cast<unsigned long long>(t + 1), main_);
-          if (split_) LSGD_CUDA(cudaEventRecord(ev_bucket_[k], main_));
-        }
+        if (split_) LSGD_CUDA(cudaEventRecord(ev_bucket_[k], main_));
       }
       phase_mark(widx(w), t, 1, 1, main_);
     }
@@ -815,8 +864,8 @@ class RankImpl final : public Rank {
     if (alg_ != LSGD_B200_LSGD) {  // sequential / csgd: synchronous update in the same block (executors.cpp:172-177)
       current_phase() = "update";
       for (auto& w : ws_) {
-        for (int b = 0; b < D; ++b) apply_bucket(w, b, t);
-        after_update(w, t);
+        for (int b = 0; b < D; ++b) apply_bucket(w, b, t, main_);
+        after_update(w, t, main_);
       }
       ++applied_;
     }
@@ -847,6 +896,8 @@ class RankImpl final : public Rank {
   bool exact_ = false, synth_ = false, split_ = false, use_tc_ = false;
   cudaStream_t main_ = nullptr, comm_ = nullptr;
   cudaEvent_t ev_bucket_[kMaxBuckets] = {};
+  cudaEvent_t ev_upd_[kMaxBuckets] = {};
+  cudaStream_t upd_ = nullptr;
   std::vector<char*> peer_base_;
   std::vector<char*> ipc_opened_;
   ncclComm_t slice_comm_ = nullptr, flat_comm_ = nullptr;

@@ -148,6 +148,16 @@ extern "C" int lsgd_b200_test_gemm(int32_t a_mn, int32_t b_mn, int32_t epi, int3
   return seam_guard([&] { tc_test_gemm(a_mn, b_mn, epi, M, N, K, 1, A, B, bias, mask, div, relu, out); });
 }
 
+extern "C" int lsgd_b200_test_gemm_timed(int32_t a_mn, int32_t b_mn, int32_t epi, int32_t M, int32_t N, int32_t K,
+                                         int32_t reps, double* avg_ms) {
+  return seam_guard([&] {
+    std::vector<float> A(static_cast<size_t>(M) * K, 0.5f), B(static_cast<size_t>(N) * K, 0.25f),
+        bias(static_cast<size_t>(N), 0.f), mask(static_cast<size_t>(M) * N, 1.f), out(static_cast<size_t>(M) * N);
+    tc_test_gemm(a_mn, b_mn, epi, M, N, K, reps, A.data(), B.data(), bias.data(), mask.data(), 512.f, 0, out.data(),
+                 avg_ms);
+  });
+}
+
 extern "C" int lsgd_b200_test_tc_step(int32_t n_layers, const int32_t* layers, int32_t batch, const float* w,
                                       const float* x, const int32_t* y, float* act, float* delta, float* grad,
                                       float* loss) {
