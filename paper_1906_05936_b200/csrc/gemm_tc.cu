@@ -81,6 +81,13 @@ __device__ __forceinline__ void tma_2d(const CUtensorMap* map, uint64_t* bar, vo
       "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void tma_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
+          "r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -130,8 +137,7 @@ __device__ __forceinline__ uint64_t op_desc(uint32_t base, int kk, const EpiPara
 template <bool MN, int R>
 __device__ __forceinline__ void load_op(const CUtensorMap* map, uint64_t* bar, uint8_t* dst, int r0, int k) {
   if (MN) {
-#pragma unroll
-    for (int c = 0; c < R / 32; ++c) tma_2d(map, bar, dst + c * MN_CHUNK_BYTES, r0 + 32 * c, k);
+    tma_3d(map, bar, dst, 0, k, r0 / 32);  // all R/32 chunks in one box (see make_map)
   } else {
     tma_2d(map, bar, dst, k, r0);
   }
@@ -458,24 +464,33 @@ struct OpView {
   bool mn;
 };
 
+// K-major operand: 2D map {K, rows}, box {BK, tile_rows}, SWIZZLE_64B.
+// MN-major operand: 3D view {32 (MN within a chunk), K, rows/32 (chunks)} with strides {ld*4 B, 128 B}, box
+// {32, BK, tile_rows/32}: one TMA brings the whole tile, chunk c landing at c * BK*128 B (the LBO of op_desc).
 CUtensorMap make_map(const OpView& v, int tile_rows) {
   CUtensorMap m;
   std::memset(&m, 0, sizeof(m));
-  cuuint64_t dims[2], strides[1];
-  cuuint32_t box[2], estr[2] = {1, 1};
+  cuuint64_t dims[3], strides[2];
+  cuuint32_t box[3], estr[3] = {1, 1, 1};
+  cuuint32_t rank = 2;
   if (v.mn) {
-    dims[0] = static_cast<cuuint64_t>(v.rows);
+    rank = 3;
+    dims[0] = 32;
     dims[1] = static_cast<cuuint64_t>(v.k);
+    dims[2] = static_cast<cuuint64_t>(v.rows / 32);
+    strides[0] = static_cast<cuuint64_t>(v.ld) * 4;
+    strides[1] = 128;
     box[0] = 32;
     box[1] = BK;
+    box[2] = static_cast<cuuint32_t>(tile_rows / 32);
   } else {
     dims[0] = static_cast<cuuint64_t>(v.k);
     dims[1] = static_cast<cuuint64_t>(v.rows);
+    strides[0] = static_cast<cuuint64_t>(v.ld) * 4;
     box[0] = BK;
     box[1] = static_cast<cuuint32_t>(tile_rows);
   }
-  strides[0] = static_cast<cuuint64_t>(v.ld) * 4;
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(v.ptr), dims, strides, box, estr,
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(v.ptr), dims, strides, box, estr,
                            CU_TENSOR_MAP_INTERLEAVE_NONE,
                            v.mn ? static_cast<CUtensorMapSwizzle>(mn_geometry().tma_swizzle) : CU_TENSOR_MAP_SWIZZLE_64B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
