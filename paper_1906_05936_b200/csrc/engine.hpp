@@ -1,15 +1,17 @@
 // The LSGD step engine (executors.cpp:190-304 re-designed for one box of B200s).
 //
-// A Rank = one host thread + one GPU + two streams (main, comm). It hosts one or more workers (one per GPU in
-// production; several when fewer GPUs than workers are visible, which emulates the ranks on one device with
-// identical arithmetic). Every worker owns a peer-visible block
-//     [flags | payload (P+1 padded to k*S) | s[0] (S) | s[1] (S) | gbar (S)]
-// which other GPUs read over NVLink (CUDA IPC when ranks are processes, direct peer pointers when threads).
-// The communicator of group g is not a separate rank: its reduction is sliced across the group's k GPUs —
-// slot j sums elements [j*S, (j+1)*S) of all members' payloads in ascending worker order (the exact order of
-// transport.cpp:27-48), so the result is bitwise the rooted reduce while each GPU moves only 2(k-1)/k of the
-// vector over NVLink. Slice owners then average across groups (NCCL on the comm stream, or the ordered peer
-// variant), and every worker pulls the k averaged slices inside the fused update kernel.
+// A Rank = one host thread + one GPU + three streams (main: io/forward/backward, comm: the communicator's
+// reduce/average/broadcast, upd: the postponed updates). It hosts one or more workers (one per GPU in production;
+// several when fewer GPUs than workers are visible, which emulates the ranks on one device with identical
+// arithmetic on a single stream). Every worker owns a peer-visible block
+//     [flags | payload | s[0] | s[1] | gbar | gfull]
+// which other GPUs read and write over NVLink (CUDA IPC when ranks are processes, direct peer pointers when
+// threads). The gradient is split into per-layer buckets (Bucket); the communicator of group g is not a separate
+// rank: each bucket's reduction is sliced across the group's k GPUs — slot j sums sub-slice j of all members'
+// payloads in ascending worker order (the exact order of transport.cpp:27-48), so the result is bitwise the rooted
+// reduce while each GPU moves only (k-1)/k of the vector over NVLink per direction. Slot owners then average
+// across groups (NCCL on the comm stream, or the ordered peer variant) and push their averaged sub-slice into every
+// member's gfull, so the update reads local HBM only.
 // Cross-GPU ordering uses monotone step counters (ld.acquire / st.release at system scope) in the peer block.
 #pragma once
 

@@ -1,13 +1,15 @@
 // tcgen05 split-TF32 GEMM for sm_100a. See gemm_tc.cuh for the numerics.
 //
-// One CTA computes a 128 x 256 fp32 tile D = A * B^T (TN form: A is M x K, B is N x K) into TMEM:
-//   warp 0      TMA producer: per 32-wide K block, boxes of A_hi, A_lo, B_hi, B_lo -> one smem stage (96 KB)
+// Persistent kernel, one CTA per SM, 128 x 256 fp32 tiles D = A * B^T (TN form: A is M x K, B is N x K) in TMEM:
+//   warp 0      TMA producer: per 16-wide K block, A_hi, A_lo, B_hi, B_lo -> one 48 KB smem stage (4-stage ring)
 //   warp 1      TMEM allocator + single-thread MMA issuer: per 8-wide K step three tcgen05.mma.kind::tf32
-//               (hi*lo, lo*hi, hi*hi) accumulate into the same 256 TMEM columns; tcgen05.commit frees the stage
-//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> fused bias/ReLU | /B | ReLU-mask, fp32 output plus the
-//               hi/lo split the next GEMM consumes
-// Operands may be K-major ([rows][K]) or MN-major ([K][rows]); both are SWIZZLE_128B canonical UMMA layouts, so
-// dX (W read MN-major) and dW (delta and activations read MN-major) need no transposed copies.
+//               (hi*lo, lo*hi, hi*hi) accumulate into one of two 256-column TMEM accumulators; tcgen05.commit
+//               frees the stage / hands the finished accumulator to the epilogue
+//   warps 2..5  epilogue (overlapping the next tile's MMAs): tcgen05.ld 32x32b -> registers -> fused bias/ReLU |
+//               /B | ReLU-mask, fp32 output plus the hi/lo split the next GEMM consumes
+// Operands may be K-major ([rows][K], TMA SWIZZLE_64B / UMMA SWIZZLE_64B) or MN-major ([K][rows], TMA
+// SWIZZLE_128B_ATOM_32B / UMMA SWIZZLE_128B_BASE32B, the only MN-major layout tf32 supports), so dX (W read
+// MN-major) and dW (delta and activations read MN-major) need no transposed copies.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -26,9 +28,9 @@ namespace {
 // BK = 16: 48 KB stages, 4 deep (the producer keeps 3 K blocks in flight ahead of the MMAs).
 constexpr int BM = 128, BN = 256, BK = 16, STAGES = 4, THREADS = 192;
 constexpr int MN_CHUNK_BYTES = BK * 128;  // one 32-wide MN chunk of an MN-major tile: BK rows of 128 B
-constexpr int A_BYTES = BM * BK * 4;                        // 16 KB
-constexpr int B_BYTES = BN * BK * 4;                        // 32 KB
-constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;      // 96 KB
+constexpr int A_BYTES = BM * BK * 4;                        // 8 KB
+constexpr int B_BYTES = BN * BK * 4;                        // 16 KB
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;      // 48 KB (hi + lo of both operands)
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;     // + alignment slack
 constexpr uint32_t TMEM_COLS = 256;
 
