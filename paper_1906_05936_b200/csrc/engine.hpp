@@ -41,10 +41,16 @@ constexpr int kArrived = 3 * kMaxBuckets;
 // Gradient buckets: one per layer (that layer's [W_k | b_k] block, contiguous in the reference's parameter
 // layout, mlp.hpp:14-18), the loss slot riding the last layer's bucket. Each bucket is split into k sub-slices of
 // S elements; sub-slice j lives in the payload at poff + j*S and in slot j's s/gbar regions at goff.
+// A large layer is split into row blocks of W_k (contiguous in the layout), so the exchange of the first blocks
+// overlaps the weight-gradient GEMMs of the later ones; the layer's bias rides its last block.
 struct Bucket {
   int64_t pstart = 0;  // first parameter index
   int64_t n = 0;       // parameters (the loss slot, when carried, is bucket-local index n)
   bool loss = false;
+  int layer = 0;       // MLP layer k
+  int row0 = 0;        // first output row of W_k in this bucket
+  int rows = 0;        // output rows of W_k in this bucket
+  bool bias = false;   // carries b_k (the layer's last block)
   int64_t S = 0;       // sub-slice length, multiple of 64 elements
   int64_t poff = 0;    // payload offset (elements, 64-aligned)
   int64_t goff = 0;    // offset inside each slot's s/gbar region (64-aligned)
@@ -54,6 +60,7 @@ struct Geometry {
   int64_t P = 0, Ppad = 0, Sg = 0;  // params, padded payload, per-slot slice elements (sum of bucket S)
   int esize = 4;
   std::vector<Bucket> buckets;
+  std::vector<std::vector<int>> layer_buckets;  // bucket indices of each layer, in row order
   int64_t loss_at = 0;             // payload index of the loss slot
   PeerLayout peer;
   Geometry(const RunSpec& spec, int elem_size);

@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 
 #include "gemm_tc.cuh"
@@ -602,6 +603,11 @@ GemmPlan make_plan(const OpView& a_hi, const float* a_lo, const OpView& b_hi, co
 struct TcLayer {
   GemmPlan fwd, wgrad, igrad;
   bool has_igrad = false;
+  // weight-gradient plans of row blocks [row0, row0 + rows) of dW_k (the engine's gradient buckets), built lazily
+  std::map<std::pair<int, int>, GemmPlan> wgrad_rows;
+  OpView dw_a, dw_b;
+  const float *dw_a_lo = nullptr, *dw_b_lo = nullptr;
+  EpiParams dw_ep{};
 };
 
 bool tc_shapes_supported(const std::vector<int32_t>& layers, int batch) {
@@ -671,6 +677,11 @@ void tc_alloc(TcWorkspace& ws, const Layout& L, int batch, int n_features) {
       ep.div = static_cast<float>(B);
       tl->wgrad = make_plan(OpView{ws.dlt_hi[di], no, B, no, true}, ws.dlt_lo[di], OpView{in_hi, ni, B, ni, true},
                             in_lo, kWgrad, ep, ws.partial, ws.partial_elems);
+      tl->dw_a = OpView{ws.dlt_hi[di], no, B, no, true};
+      tl->dw_a_lo = ws.dlt_lo[di];
+      tl->dw_b = OpView{in_hi, ni, B, ni, true};
+      tl->dw_b_lo = in_lo;
+      tl->dw_ep = ep;
     }
     // input grad: delta_{k-1}[B, ni] = (delta_k[B, no] . W_k[no, ni]) * [act_{k-1} > 0]  (W read MN-major)
     if (k > 0) {
@@ -734,17 +745,44 @@ void tc_head(TcWorkspace& ws, const Layout& L, const int32_t* y, float* sample_l
   launch_mean_loss<float>(sample_loss, B, loss_out, st, lc);
 }
 
-void tc_backward_layer(TcWorkspace& ws, const Layout& L, int k, float* gW, float* gb, cudaStream_t st,
-                       LaunchCounter& lc) {
+void tc_backward_dw(TcWorkspace& ws, const Layout& L, int k, int row0, int rows, float* gW, cudaStream_t st,
+                    LaunchCounter& lc) {
+  (void)L;
   TcLayer* tl = ws.layers[static_cast<size_t>(k)];
-  const int di = (L.depth() - 1 - k) & 1;
-  GemmPlan pw = tl->wgrad;
+  auto key = std::make_pair(row0, rows);
+  auto it = tl->wgrad_rows.find(key);
+  if (it == tl->wgrad_rows.end()) {
+    OpView a = tl->dw_a;  // rows of dW_k are the MN (out) index of delta_k
+    a.ptr += row0;
+    a.rows = rows;
+    OpView alo = a;
+    alo.ptr = tl->dw_a_lo + row0;
+    it = tl->wgrad_rows.emplace(key, make_plan(a, alo.ptr, tl->dw_b, tl->dw_b_lo, kWgrad, tl->dw_ep, ws.partial,
+                                               ws.partial_elems)).first;
+  }
+  GemmPlan pw = it->second;
   pw.ep.out = gW;
   run_plan(pw, st, lc);
+}
+
+void tc_backward_bias(TcWorkspace& ws, const Layout& L, int k, float* gb, cudaStream_t st, LaunchCounter& lc) {
+  const int di = (L.depth() - 1 - k) & 1;
   bias_grad_f32_kernel<<<(L.out(k) + 31) / 32, dim3(32, 8), 0, st>>>(ws.dlt[di], ws.batch, L.out(k), gb);
   ++lc.n;
   LSGD_CUDA(cudaGetLastError());
+}
+
+void tc_backward_dx(TcWorkspace& ws, const Layout& L, int k, cudaStream_t st, LaunchCounter& lc) {
+  (void)L;
+  TcLayer* tl = ws.layers[static_cast<size_t>(k)];
   if (tl->has_igrad) run_plan(tl->igrad, st, lc);
+}
+
+void tc_backward_layer(TcWorkspace& ws, const Layout& L, int k, float* gW, float* gb, cudaStream_t st,
+                       LaunchCounter& lc) {
+  tc_backward_dw(ws, L, k, 0, L.out(k), gW, st, lc);
+  tc_backward_bias(ws, L, k, gb, st, lc);
+  tc_backward_dx(ws, L, k, st, lc);
 }
 
 void tc_test_gemm(int a_mn, int b_mn, int epi, int M, int N, int K, int reps, const float* A, const float* Bm,

@@ -50,6 +50,11 @@ void tc_head(TcWorkspace& ws, const Layout& L, const int32_t* y, float* sample_l
 // Backward layer k: dW_k -> gW ([out x in], /B), db_k -> gb, and (k > 0) the masked delta of layer k-1.
 void tc_backward_layer(TcWorkspace& ws, const Layout& L, int k, float* gW, float* gb, cudaStream_t st,
                        LaunchCounter& lc);
+// The same in pieces: rows [row0, row0+rows) of dW_k -> gW (row stride in_k), then db_k, then dX_k.
+void tc_backward_dw(TcWorkspace& ws, const Layout& L, int k, int row0, int rows, float* gW, cudaStream_t st,
+                    LaunchCounter& lc);
+void tc_backward_bias(TcWorkspace& ws, const Layout& L, int k, float* gb, cudaStream_t st, LaunchCounter& lc);
+void tc_backward_dx(TcWorkspace& ws, const Layout& L, int k, cudaStream_t st, LaunchCounter& lc);
 
 // Standalone GEMM for conformance tests: D = A * B^T with A [M x K], B [N x K] given in their storage major
 // (K-major: [rows][K]; MN-major: [K][rows]), epilogue 0 forward (bias, relu), 1 weight-grad (/div), 2 input-grad

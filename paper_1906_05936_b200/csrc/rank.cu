@@ -11,6 +11,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -44,13 +46,33 @@ Geometry::Geometry(const RunSpec& spec, int es) : esize(es) {
     Layout L(spec.layers);
     P = L.n_params;
     check<ConfigError>(L.depth() <= kMaxBuckets, "at most ", kMaxBuckets, " layers are supported");
+    // Row blocks of ~64 MB (fp32) per bucket, block heights a multiple of the 128-row GEMM tile.
+    // LSGD_B200_BUCKET_ELEMS overrides the target (tests force multi-block buckets on small models).
+    const char* env = std::getenv("LSGD_B200_BUCKET_ELEMS");
+    const double kBucketElems = env ? std::max(1.0, std::atof(env)) : 16.0 * 1024 * 1024;
+    layer_buckets.resize(static_cast<size_t>(L.depth()));
     for (int k = 0; k < L.depth(); ++k) {
-      Bucket b;
-      b.pstart = L.w_off[static_cast<size_t>(k)];
-      b.n = static_cast<int64_t>(L.in(k)) * L.out(k) + L.out(k);
-      buckets.push_back(b);
+      const int in = L.in(k), out = L.out(k);
+      int nc = std::max(1, static_cast<int>(std::ceil(static_cast<double>(in) * out / kBucketElems)));
+      const int quantum = out % 128 == 0 ? 128 : (out % 8 == 0 ? 8 : out);  // GEMM tile rows
+      while (nc > 1 && (out % nc != 0 || (out / nc) % quantum != 0)) --nc;
+      const int rows = out / nc;
+      for (int c = 0; c < nc; ++c) {
+        Bucket b;
+        b.layer = k;
+        b.row0 = c * rows;
+        b.rows = rows;
+        b.bias = c + 1 == nc;
+        b.pstart = L.w_off[static_cast<size_t>(k)] + static_cast<int64_t>(b.row0) * in;
+        b.n = static_cast<int64_t>(rows) * in + (b.bias ? out : 0);
+        layer_buckets[static_cast<size_t>(k)].push_back(static_cast<int>(buckets.size()));
+        buckets.push_back(b);
+      }
     }
+    check<ConfigError>(static_cast<int>(buckets.size()) <= kMaxBuckets, "model too large: more than ", kMaxBuckets,
+                       " gradient buckets");
   }
+  if (layer_buckets.empty()) layer_buckets.push_back({0});
   buckets.back().loss = true;
   const int k = spec.k();
   int64_t poff = 0, goff = 0;
@@ -661,27 +683,43 @@ class RankImpl final : public Rank {
     launch_mean_loss<T>(w.sample_loss, B_, loss_out, main_, lc_);
   }
 
-  void backward_layer(Worker& w, int k) {
-    if (synth_) return;
-    Timed tm(this, "gemm", main_);
-    const Bucket& bk = geo_.buckets[static_cast<size_t>(k)];
+  // Weight gradient of bucket b (a row block of dW_k, plus db_k for the layer's last block).
+  void backward_bucket(Worker& w, int b) {
+    const Bucket& bk = geo_.buckets[static_cast<size_t>(b)];
+    const int k = bk.layer;
     const int ni = L_.in(k), no = L_.out(k);
     T* gW = w.payload + bk.poff;
-    T* gb = gW + static_cast<int64_t>(ni) * no;
+    T* gb = gW + static_cast<int64_t>(bk.rows) * ni;
+    Timed tm(this, "gemm", main_);
     if (use_tc_) {
-      tc_backward_layer(w.tc, L_, k, reinterpret_cast<float*>(gW), reinterpret_cast<float*>(gb), main_, lc_);
+      tc_backward_dw(w.tc, L_, k, bk.row0, bk.rows, reinterpret_cast<float*>(gW), main_, lc_);
+      if (bk.bias) tc_backward_bias(w.tc, L_, k, reinterpret_cast<float*>(gb), main_, lc_);
       return;
     }
-    T* dcur = delta_buf(w, k);
+    const T* dcur = delta_buf(w, k);
     const T* aprev = k == 0 ? w.x : w.act[static_cast<size_t>(k - 1)];
-    launch_gemm_simt<T>(kEpiWeightGrad, exact_, no, ni, B_, dcur, 1, no, aprev, ni, 1, gW, ni, nullptr, 0,
-                        static_cast<T>(B_), nullptr, main_, lc_);
-    launch_bias_grad<T>(dcur, B_, no, gb, main_, lc_);
-    if (k > 0) {
-      const T* Wk = w.w + L_.w_off[static_cast<size_t>(k)];
-      launch_gemm_simt<T>(kEpiInputGrad, exact_, B_, ni, no, dcur, no, 1, Wk, ni, 1, delta_buf(w, k - 1), ni, nullptr, 0,
-                          T(0), w.act[static_cast<size_t>(k - 1)], main_, lc_);
+    launch_gemm_simt<T>(kEpiWeightGrad, exact_, bk.rows, ni, B_, dcur + bk.row0, 1, no, aprev, ni, 1, gW, ni, nullptr,
+                        0, static_cast<T>(B_), nullptr, main_, lc_);
+    if (bk.bias) launch_bias_grad<T>(dcur, B_, no, gb, main_, lc_);
+  }
+
+  // Input gradient of layer k (masked delta of layer k-1); layer 0 has none (mlp.cpp:116).
+  void backward_input(Worker& w, int k) {
+    if (k == 0) return;
+    Timed tm(this, "gemm", main_);
+    if (use_tc_) {
+      tc_backward_dx(w.tc, L_, k, main_, lc_);
+      return;
     }
+    const int ni = L_.in(k), no = L_.out(k);
+    const T* Wk = w.w + L_.w_off[static_cast<size_t>(k)];
+    launch_gemm_simt<T>(kEpiInputGrad, exact_, B_, ni, no, delta_buf(w, k), no, 1, Wk, ni, 1, delta_buf(w, k - 1), ni,
+                        nullptr, 0, T(0), w.act[static_cast<size_t>(k - 1)], main_, lc_);
+  }
+
+  void backward_layer(Worker& w, int k) {  // compute_gradient (kernel seam): all blocks, then dX
+    for (int b : geo_.layer_buckets[static_cast<size_t>(k)]) backward_bucket(w, b);
+    backward_input(w, k);
   }
 
   std::vector<int> group_members(int g) const {
@@ -787,63 +825,81 @@ class RankImpl final : public Rank {
   // ------------------------------------------------------------------------------------------ one step
   void issue_one(int64_t t, const int32_t* given, bool shard_only) {
     const int D = synth_ ? 1 : L_.depth();
+    const int NB = nb_;
+    const auto& LB = geo_.layer_buckets;
     current_phase() = "io";
     if (!synth_) io(t, given, shard_only);
     else launch_sleep(spec_.c.io_delay_s, main_, lc_);
 
     // postponed update of round t-1, bucket by bucket, each finished right before the forward of its layer.
-    // One worker per rank: the updates run on their own stream, so bucket k+1's update (waiting for its averaged
-    // gradient, then streaming w/v through HBM) overlaps the forward GEMM of layer k.
+    // One worker per rank: the updates run on their own stream, so the next layer's update (waiting for its averaged
+    // gradient, then streaming w/v through HBM) overlaps the forward GEMM of the current layer.
     const bool postponed = alg_ == LSGD_B200_LSGD && t >= 1;
     if (postponed && split_) {
       Worker& w = ws_[0];
       current_phase() = "broadcast";
-      for (int k = 0; k < D; ++k) {
-        if (reduce_folded()) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_bucket_[k], 0));  // payload k of round t-1
-        apply_bucket(w, k, t - 1, upd_);
-        LSGD_CUDA(cudaEventRecord(ev_upd_[k], upd_));
+      for (int b = 0; b < NB; ++b) {
+        if (reduce_folded()) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_bucket_[b], 0));  // payload b of round t-1
+        apply_bucket(w, b, t - 1, upd_);
+        LSGD_CUDA(cudaEventRecord(ev_upd_[b], upd_));
       }
       after_update(w, t - 1, upd_);
     }
+    const bool exchange = !flat_nccl() && !reduce_folded() && alg_ != LSGD_B200_SEQUENTIAL;
     for (auto& w : ws_) {
       current_phase() = "compute";
       phase_mark(widx(w), t, 1, 0, main_);
       for (int k = 0; k < D; ++k) {
-        if (postponed && split_) {
-          LSGD_CUDA(cudaStreamWaitEvent(main_, ev_upd_[k], 0));
-        } else if (postponed) {
-          current_phase() = "broadcast";
-          apply_bucket(w, k, t - 1, main_);
-          current_phase() = "compute";
+        for (int b : LB[static_cast<size_t>(k)]) {
+          if (postponed && split_) {
+            LSGD_CUDA(cudaStreamWaitEvent(main_, ev_upd_[b], 0));
+          } else if (postponed) {
+            current_phase() = "broadcast";
+            apply_bucket(w, b, t - 1, main_);
+            current_phase() = "compute";
+          }
         }
         forward_layer(w, k);
       }
       if (postponed && !split_) after_update(w, t - 1, main_);
       head(w);
       for (int k = D - 1; k >= 0; --k) {
-        backward_layer(w, k);
-        if (!flat_nccl() && !reduce_folded() && alg_ != LSGD_B200_SEQUENTIAL)
-          signal(w, kFlagGrad, k, static_cast<unsigned long long>(t + 1), main_);
-        if (split_) LSGD_CUDA(cudaEventRecord(ev_bucket_[k], main_));
+        if (!synth_) {
+          for (int b : LB[static_cast<size_t>(k)]) {
+            backward_bucket(w, b);  // row block of dW_k (+ db_k): ready for the exchange right away
+            if (exchange) signal(w, kFlagGrad, b, static_cast<unsigned long long>(t + 1), main_);
+            if (split_) LSGD_CUDA(cudaEventRecord(ev_bucket_[b], main_));
+          }
+          backward_input(w, k);
+        } else {
+          if (exchange) signal(w, kFlagGrad, 0, static_cast<unsigned long long>(t + 1), main_);
+          if (split_) LSGD_CUDA(cudaEventRecord(ev_bucket_[0], main_));
+        }
       }
       phase_mark(widx(w), t, 1, 1, main_);
     }
     if (postponed) ++applied_;
 
-    // communicator work: per bucket in backward order, on the comm stream (overlapping the rest of the backward)
+    // exchange order: the order buckets finish in the backward (layers descending, row blocks ascending)
+    std::vector<int> order;
+    for (int k = D - 1; k >= 0; --k)
+      for (int b : LB[static_cast<size_t>(k)]) order.push_back(b);
+
+    // communicator work: per bucket, on the comm stream (overlapping the rest of the backward)
     current_phase() = "local_reduce";
     if (flat_nccl()) {
       Timed tm(this, "global", main_);
       for (auto& w : ws_)
         LSGD_NCCL(ncclAllReduce(w.payload, w.payload, static_cast<size_t>(geo_.Ppad), nccl_type(), ncclSum,
                                 flat_comm_, main_));
-    } else if (!reduce_folded() && alg_ != LSGD_B200_SEQUENTIAL) {
+    } else if (exchange) {
       for (auto& w : ws_) phase_mark(widx(w), t, 2, 0, comm_);
       if (split_) {
         Worker& w = ws_[0];
-        for (int b = D - 1; b >= 0; --b) {
+        for (size_t q = 0; q < order.size(); ++q) {
+          const int b = order[q];
           LSGD_CUDA(cudaStreamWaitEvent(comm_, ev_bucket_[b], 0));
-          if (b == D - 1) launch_sleep(spec_.c.global_link_delay_s, comm_, lc_);
+          if (q == 0) launch_sleep(spec_.c.global_link_delay_s, comm_, lc_);
           reduce_bucket(w, b, t, comm_);
           current_phase() = "global_allreduce";
           global_bucket(w, b, t, comm_);
@@ -851,11 +907,11 @@ class RankImpl final : public Rank {
         }
       } else {
         // emulated ranks share one stream: every local slice sum is published before any global average waits
-        for (int b = D - 1; b >= 0; --b)
+        for (int b : order)
           for (auto& w : ws_) reduce_bucket(w, b, t, main_);
         current_phase() = "global_allreduce";
         launch_sleep(spec_.c.global_link_delay_s, main_, lc_);
-        for (int b = D - 1; b >= 0; --b)
+        for (int b : order)
           for (auto& w : ws_) global_bucket(w, b, t, main_);
       }
       for (auto& w : ws_) phase_mark(widx(w), t, 3, 1, comm_);
@@ -864,7 +920,7 @@ class RankImpl final : public Rank {
     if (alg_ != LSGD_B200_LSGD) {  // sequential / csgd: synchronous update in the same block (executors.cpp:172-177)
       current_phase() = "update";
       for (auto& w : ws_) {
-        for (int b = 0; b < D; ++b) apply_bucket(w, b, t, main_);
+        for (int b = 0; b < NB; ++b) apply_bucket(w, b, t, main_);
         after_update(w, t, main_);
       }
       ++applied_;

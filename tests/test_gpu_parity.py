@@ -229,3 +229,22 @@ def test_multi_gpu_matches_reference(name, glob, n_gpus):
     cfg.b200.n_devices = 1  # emulated ranks on one GPU give the same bits (G <= 2: NCCL's a+b commutes)
     r1 = lsgd.run_train(cfg)
     assert np.array_equal(r1.final_params.view(np.uint64), r.final_params.view(np.uint64))
+
+
+@pytest.mark.parametrize("dtype,tol", [("fp64", FP64_TOL), ("fp32", FP32_TOL)])
+def test_row_block_buckets_keep_parity(dtype, tol, monkeypatch):
+    """Large layers are exchanged in row blocks (sub-buckets); force several blocks on a small model and check the
+    reference iterates are unchanged (per-coordinate in fp64, norm-wise in fp32)."""
+    monkeypatch.setenv("LSGD_B200_BUCKET_ELEMS", "100")
+    cfg = lsgd.TrainConfig(algorithm="lsgd", n_workers=4, n_groups=2, layer_sizes=[16, 64, 32, 4], n_samples=512,
+                           n_features=16, n_classes=4, spread=6.0, mode="momentum", local_batch=8, iterations=12,
+                           record_history=True)
+    cfg.b200.dtype = dtype
+    cfg.b200.n_devices = 1
+    cfg.b200.global_allreduce = "ordered"
+    r = lsgd.run_train(cfg)
+    from oracle import Oracle, TrainSpec
+    spec = TrainSpec(**{k: getattr(cfg, k) for k in TrainSpec.__dataclass_fields__ if hasattr(cfg, k)})
+    ref = Oracle("port").run_train(spec, history=True)["history"]
+    e = compare_histories(ref, r.param_history, "blocks")
+    assert (e.max_rel_deviation if dtype == "fp64" else e.max_normwise_deviation) <= tol, e
