@@ -150,6 +150,9 @@ int lsgd_b200_rank_drain(lsgd_b200_rank* r);
 int lsgd_b200_rank_synchronize(lsgd_b200_rank* r);
 /* Loss of the most recent applied round, read back from the device (D2H of one element). */
 int lsgd_b200_rank_last_loss(lsgd_b200_rank* r, double* loss);
+/* Non-blocking variant: enqueue the D2H copy of that loss (float for fp32, double for fp64; *elem_bytes says
+ * which) into caller-owned pinned memory, ordered after the round's update; valid after the next synchronize. */
+int lsgd_b200_rank_loss_async(lsgd_b200_rank* r, void* host_pinned, int32_t* elem_bytes);
 int lsgd_b200_rank_get_params(lsgd_b200_rank* r, double* w, int64_t n);
 int lsgd_b200_rank_set_params(lsgd_b200_rank* r, const double* w, int64_t n);
 /* Losses / lrs of applied rounds [0, n) (device history, D2H). */
@@ -157,6 +160,9 @@ int lsgd_b200_rank_history(lsgd_b200_rank* r, double* loss, double* lr, int64_t 
 /* Kernels this rank has launched so far, and its CUDA stream (cudaStream_t) for event timing. */
 int lsgd_b200_rank_launches(lsgd_b200_rank* r, int64_t* out);
 int lsgd_b200_rank_stream(lsgd_b200_rank* r, void** stream);
+/* Make that stream wait (device-side, no host sync) for all work issued so far on the rank's side streams
+ * (communicator, update, host-row copies), so an event recorded on it after this call closes the issued steps. */
+int lsgd_b200_rank_join(lsgd_b200_rank* r);
 /* Device-timed average duration (ms) of the named kernel family over the launches since the last reset,
  * measured with CUDA events on the launching stream. family: "gemm", "reduce", "update", "global". */
 int lsgd_b200_rank_kernel_time(lsgd_b200_rank* r, const char* family, double* avg_ms, int64_t* count);

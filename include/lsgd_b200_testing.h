@@ -27,6 +27,11 @@ int lsgd_b200_test_gemm_timed(int32_t a_mn, int32_t b_mn, int32_t epi, int32_t M
 int lsgd_b200_test_tc_step(int32_t n_layers, const int32_t* layers, int32_t batch, const float* w, const float* x,
                            const int32_t* y, float* act, float* delta, float* grad, float* loss);
 
+/* Every launch timed since lsgd_b200_rank_timing(r, 1), one "family<TAB>start_ms<TAB>end_ms" line each (device
+ * clock via CUDA events, relative to the timing call), into buf (NUL-terminated, truncated to cap). */
+typedef struct lsgd_b200_rank lsgd_b200_rank;
+int lsgd_b200_test_rank_timeline(lsgd_b200_rank* r, char* buf, int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,6 +82,8 @@ _SIGNATURES = {
     "lsgd_b200_rank_drain": ([_P], C.c_int),
     "lsgd_b200_rank_synchronize": ([_P], C.c_int),
     "lsgd_b200_rank_last_loss": ([_P, _P], C.c_int),
+    "lsgd_b200_rank_loss_async": ([_P, _P, _P], C.c_int),
+    "lsgd_b200_rank_join": ([_P], C.c_int),
     "lsgd_b200_rank_get_params": ([_P, _P, C.c_int64], C.c_int),
     "lsgd_b200_rank_set_params": ([_P, _P, C.c_int64], C.c_int),
     "lsgd_b200_rank_history": ([_P, _P, _P, C.c_int64], C.c_int),

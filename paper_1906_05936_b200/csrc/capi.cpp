@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -325,8 +326,26 @@ int lsgd_b200_rank_launches(lsgd_b200_rank* r, int64_t* out) {
 int lsgd_b200_rank_stream(lsgd_b200_rank* r, void** stream) {
   return guarded([&] { *stream = r->rank->main_stream(); });
 }
+int lsgd_b200_rank_join(lsgd_b200_rank* r) {
+  return guarded([&] { r->rank->join(); });
+}
 int lsgd_b200_rank_kernel_time(lsgd_b200_rank* r, const char* family, double* avg_ms, int64_t* count) {
   return guarded([&] { r->rank->kernel_time(family, avg_ms, count); });
+}
+int lsgd_b200_rank_loss_async(lsgd_b200_rank* r, void* host_pinned, int32_t* elem_bytes) {
+  return guarded([&] {
+    const int n = r->rank->loss_async(host_pinned);
+    if (elem_bytes) *elem_bytes = n;
+  });
+}
+int lsgd_b200_test_rank_timeline(lsgd_b200_rank* r, char* buf, int64_t cap) {
+  return guarded([&] {
+    const std::string t = r->rank->timeline();
+    check<Error>(cap > 0, "timeline buffer is empty");
+    const size_t n = std::min(t.size(), static_cast<size_t>(cap - 1));
+    std::memcpy(buf, t.data(), n);
+    buf[n] = '\0';
+  });
 }
 int lsgd_b200_rank_timing(lsgd_b200_rank* r, int32_t enable) {
   return guarded([&] { r->rank->set_timing(enable != 0); });

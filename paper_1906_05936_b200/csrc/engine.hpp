@@ -89,10 +89,15 @@ class Rank {
   virtual void param_history(double* out, int64_t rows) = 0;   // worker0 w_0..w_{rows-1}
   virtual void phase_spans(int worker, double* out, int64_t T) = 0;
   virtual double last_loss() = 0;
+  // Enqueue the D2H copy of the latest applied round's loss into pinned host memory; returns its size in bytes.
+  virtual int loss_async(void* host_pinned) = 0;
   virtual int64_t launches() const = 0;
   virtual void* main_stream() = 0;
+  virtual void join() = 0;  // main_stream waits for everything issued so far on the rank's other streams
   virtual void set_timing(bool on) = 0;
   virtual void kernel_time(const std::string& family, double* avg_ms, int64_t* count) = 0;
+  // Every timed launch since set_timing(true) as "family<TAB>start_ms<TAB>end_ms" lines (relative to that call).
+  virtual std::string timeline() = 0;
   // Kernel seam (batch_gradient, mlp.hpp:54): gather `idx`, forward/backward, return grad [P] and mean loss.
   virtual void compute_gradient(const int32_t* idx, double* grad, double* loss) = 0;
   virtual void abort() = 0;

@@ -26,14 +26,24 @@ namespace lsgd_b200 {
 
 namespace {
 
-// BK = 16: 48 KB stages, 4 deep (the producer keeps 3 K blocks in flight ahead of the MMAs).
-constexpr int BM = 128, BN = 256, BK = 16, STAGES = 4, THREADS = 192;
+// BK = 16. PAIR = 1: one CTA per 128 x 256 tile, 48 KB stages x 4. PAIR = 2 (cta_group::2): a CTA pair computes a
+// 256 x 256 tile, each CTA staging its 128 rows of A and half (128 rows) of B -> 32 KB stages x 6; per MMA flop the
+// pair moves 1/3 fewer bytes from L2 than two single CTAs (the 1-CTA kernel is L2-throughput bound).
+constexpr int BM = 128, BN = 256, BK = 16, THREADS = 192;
 constexpr int MN_CHUNK_BYTES = BK * 128;  // one 32-wide MN chunk of an MN-major tile: BK rows of 128 B
-constexpr int A_BYTES = BM * BK * 4;                        // 8 KB
-constexpr int B_BYTES = BN * BK * 4;                        // 16 KB
-constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;      // 48 KB (hi + lo of both operands)
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;     // + alignment slack
+constexpr int A_BYTES = BM * BK * 4;      // 8 KB
+constexpr int STAGE_RING_BYTES = 192 * 1024;
+template <int PAIR>
+struct Cfg {
+  static constexpr int B_ROWS = BN / PAIR;                          // B rows staged by one CTA
+  static constexpr int B_BYTES = B_ROWS * BK * 4;                   // 16 KB | 8 KB
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;     // 48 KB | 32 KB (hi + lo of both operands)
+  static constexpr int STAGES = STAGE_RING_BYTES / STAGE_BYTES;     // 4 | 6
+};
+constexpr int EPI_STAGE_BYTES = 32 * 32 * 4;  // per epilogue warp: one 32 x 32 fp32 chunk (4 KB)
+constexpr int SMEM_BYTES = STAGE_RING_BYTES + 4 * EPI_STAGE_BYTES + 1024;  // + alignment slack
 constexpr uint32_t TMEM_COLS = 256;
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // clears the CTA-rank bit of a shared::cluster address -> leader CTA
 
 enum : int { kFwd = 0, kWgrad = 1, kIgrad = 2, kRaw = 3 };
 
@@ -53,6 +63,7 @@ struct EpiParams {
   uint32_t prefetch;                   // prefetch.tensormap the four operand maps
   int div_pow2;                        // div is a power of two: multiply by the exact reciprocal
   float div_inv;
+  uint32_t probe;  // bring-up/tuning only (LSGD_TC_PROBE): 1 skip epilogue stores, 2 skip MMAs, 4 skip TMA loads
 };
 
 // ------------------------------------------------------------------------------------------ PTX helpers
@@ -91,6 +102,29 @@ __device__ __forceinline__ void tma_3d(const CUtensorMap* map, uint64_t* bar, vo
       "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// cta_group::2 TMA: data lands in the issuing CTA's smem, the byte count completes on the leader's barrier.
+__device__ __forceinline__ void tma_2d_pair(const CUtensorMap* map, uint32_t bar, void* dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d_pair(const CUtensorMap* map, uint32_t bar, void* dst, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5}], [%2];" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -100,6 +134,22 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accum) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+// Arrive on the barrier at this offset in both CTAs of the pair once the issued MMAs complete.
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .b16 m;\n mov.b16 m, 3;\n"
+      " tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}\n" ::"r"(
+          su32(bar))
       : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -121,9 +171,9 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
 }
 
 // Instruction descriptor: D f32, A/B tf32, majors, N>>3, M>>4.
-__host__ __device__ constexpr uint32_t idesc_tf32(bool a_mn, bool b_mn) {
+__host__ __device__ constexpr uint32_t idesc_tf32(bool a_mn, bool b_mn, int m) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
-         (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(BM >> 4) << 24);
+         (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
 }
 
 // Descriptor of operand tile `base` (R rows/cols of MN, 32 K) for the kk-th 8-wide K step.
@@ -137,9 +187,13 @@ __device__ __forceinline__ uint64_t op_desc(uint32_t base, int kk, const EpiPara
 }
 
 // TMA of one operand tile (R along M/N) for K block starting at k.
-template <bool MN, int R>
+template <bool MN, int PAIR>
 __device__ __forceinline__ void load_op(const CUtensorMap* map, uint64_t* bar, uint8_t* dst, int r0, int k) {
-  if (MN) {
+  if (PAIR == 2) {
+    const uint32_t lead = su32(bar) & kPeerMask;
+    if (MN) tma_3d_pair(map, lead, dst, 0, k, r0 / 32);
+    else tma_2d_pair(map, lead, dst, k, r0);
+  } else if (MN) {
     tma_3d(map, bar, dst, 0, k, r0 / 32);  // all R/32 chunks in one box (see make_map)
   } else {
     tma_2d(map, bar, dst, k, r0);
@@ -152,52 +206,59 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float(r);
 }
 
-__device__ __forceinline__ void epi_store(const EpiParams& ep, int epi, int row, int col0, const float* v32) {
-  // 32 consecutive columns of one row
+// Epilogue on 4 consecutive columns [col, col + 4) of one row (coalesced: the lanes of a warp cover whole 128 B
+// rows). aux = b[col..col+3] (forward) or the ReLU mask source act[row][col..col+3] (input gradient), loaded by the
+// caller ahead of time (epi_aux) so its latency overlaps the previous chunk.
+__device__ __forceinline__ float4 epi_aux(const EpiParams& ep, int epi, int row, int col) {
+  if (epi == kFwd) return __ldg(reinterpret_cast<const float4*>(ep.bias + col));
+  if (epi == kIgrad) return __ldg(reinterpret_cast<const float4*>(ep.mask + static_cast<int64_t>(row) * ep.ldm + col));
+  return make_float4(0.f, 0.f, 0.f, 0.f);
+}
+__device__ __forceinline__ void epi_vec4(const EpiParams& ep, int epi, int row, int col, float4 v, float4 aux) {
+  const float4 bias4 = aux;
   if (epi == kRaw) {
-    float* p = ep.partial + static_cast<int64_t>(row) * ep.N + col0;
-#pragma unroll
-    for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(v32[i], v32[i + 1], v32[i + 2], v32[i + 3]);
+    *reinterpret_cast<float4*>(ep.partial + static_cast<int64_t>(row) * ep.N + col) = v;
     return;
   }
-  float o[32];
+  float o[4] = {v.x, v.y, v.z, v.w};
+  if (epi == kFwd) {
+    const float b[4] = {bias4.x, bias4.y, bias4.z, bias4.w};
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    float v = v32[i];
-    if (epi == kFwd) {
-      v = __fadd_rn(v, __ldg(ep.bias + col0 + i));
-      if (ep.relu && v < 0.f) v = 0.f;
-    } else if (epi == kWgrad) {
-      v = ep.div_pow2 ? v * ep.div_inv : __fdiv_rn(v, ep.div);  // x * 2^-k is exactly x / 2^k
-    } else {
-      if (!(__ldg(ep.mask + static_cast<int64_t>(row) * ep.ldm + col0 + i) > 0.f)) v = 0.f;
+    for (int i = 0; i < 4; ++i) {
+      o[i] = __fadd_rn(o[i], b[i]);
+      if (ep.relu && o[i] < 0.f) o[i] = 0.f;
     }
-    o[i] = v;
+  } else if (epi == kWgrad) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = ep.div_pow2 ? o[i] * ep.div_inv : __fdiv_rn(o[i], ep.div);  // x*2^-k == x/2^k
+  } else {
+    const float mk[4] = {aux.x, aux.y, aux.z, aux.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (!(mk[i] > 0.f)) o[i] = 0.f;
   }
-  float* p = ep.out + static_cast<int64_t>(row) * ep.ldo + col0;
-#pragma unroll
-  for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]);
+  const int64_t at = static_cast<int64_t>(row) * ep.ldo + col;
+  *reinterpret_cast<float4*>(ep.out + at) = make_float4(o[0], o[1], o[2], o[3]);
   if (ep.out_hi) {
-    float* ph = ep.out_hi + static_cast<int64_t>(row) * ep.ldo + col0;
-    float* pl = ep.out_lo + static_cast<int64_t>(row) * ep.ldo + col0;
-#pragma unroll
-    for (int i = 0; i < 32; i += 4) {
-      float h0 = tf32_rna(o[i]), h1 = tf32_rna(o[i + 1]), h2 = tf32_rna(o[i + 2]), h3 = tf32_rna(o[i + 3]);
-      *reinterpret_cast<float4*>(ph + i) = make_float4(h0, h1, h2, h3);
-      *reinterpret_cast<float4*>(pl + i) = make_float4(tf32_rna(o[i] - h0), tf32_rna(o[i + 1] - h1),
-                                                       tf32_rna(o[i + 2] - h2), tf32_rna(o[i + 3] - h3));
-    }
+    const float h0 = tf32_rna(o[0]), h1 = tf32_rna(o[1]), h2 = tf32_rna(o[2]), h3 = tf32_rna(o[3]);
+    *reinterpret_cast<float4*>(ep.out_hi + at) = make_float4(h0, h1, h2, h3);
+    *reinterpret_cast<float4*>(ep.out_lo + at) =
+        make_float4(tf32_rna(o[0] - h0), tf32_rna(o[1] - h1), tf32_rna(o[2] - h2), tf32_rna(o[3] - h3));
   }
 }
 
-// Persistent: grid = min(tiles, SMs); CTA c takes tiles c, c + grid, ... (m fastest, so the CTAs working at the
-// same time share B tiles in L2). Two TMEM accumulators (2 x 256 columns) let the epilogue of tile i overlap the
-// MMAs of tile i+1; the smem stage ring runs continuously across tiles.
-template <bool A_MN, bool B_MN>
+// Persistent: one CTA (PAIR = 1) or CTA pair (PAIR = 2, a 2-CTA cluster) per tile slot; slot c takes tiles c,
+// c + slots, ... (m fastest, so the slots working at the same time share B tiles in L2). Two TMEM accumulators
+// (2 x 256 columns) let the epilogue of tile i overlap the MMAs of tile i+1; the smem stage ring runs continuously
+// across tiles. In pair mode the leader CTA (rank 0) issues the cta_group::2 MMAs and owns the full/tmem-empty
+// barriers; both CTAs load their halves, and the MMA commits multicast to both CTAs' empty/tmem-full barriers.
+template <bool A_MN, bool B_MN, int PAIR>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                        const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo, int epi,
                        int k_per_split, int splits, EpiParams ep) {
+  using C = Cfg<PAIR>;
+  constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ alignas(8) uint64_t full_bar[STAGES];
@@ -207,7 +268,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   __shared__ uint32_t tmem_slot;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int mt = ep.M / BM, nt = ep.N / BN;
+  const uint32_t rank = PAIR == 2 ? cluster_rank() : 0u;
+  const int slot = blockIdx.x / PAIR, nslots = gridDim.x / PAIR;
+  const int mt = ep.M / (BM * PAIR), nt = ep.N / BN;
   const int tiles = mt * nt * splits;
   const int nkb = k_per_split / BK;
 
@@ -218,7 +281,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 4);  // one arrival per epilogue warp
+      mbar_init(&tempty_bar[a], 4 * PAIR);  // one arrival per epilogue warp of each CTA
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (ep.prefetch) {
@@ -229,79 +292,109 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_slot)),
-                 "r"(2 * TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (PAIR == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_slot)),
+                   "r"(2 * TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_slot)),
+                   "r"(2 * TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR == 2) cluster_sync_all();  // the peer's barriers are initialised before any remote arrive / TMA
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
       uint32_t it = 0;  // k-blocks issued by this CTA across all its tiles (stage ring position)
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int t = slot; t < tiles; t += nslots) {
         const int z = t / (mt * nt), r = t % (mt * nt);
-        const int m0 = (r % mt) * BM, n0 = (r / mt) * BN, k0 = z * k_per_split;
+        const int m0 = (r % mt) * BM * PAIR + static_cast<int>(rank) * BM;
+        const int n0 = (r / mt) * BN + static_cast<int>(rank) * C::B_ROWS, k0 = z * k_per_split;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
           if (it >= STAGES) mbar_wait(&empty_bar[s], ph ^ 1u);
-          uint8_t* st = smem + s * STAGE_BYTES;
-          mbar_expect_tx(&full_bar[s], STAGE_BYTES);
+          uint8_t* st = smem + s * C::STAGE_BYTES;
+          if (ep.probe & 4u) {
+            if (rank == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full_bar[s])) : "memory");
+            continue;
+          }
+          if (rank == 0) mbar_expect_tx(&full_bar[s], C::STAGE_BYTES * PAIR);  // the leader counts both halves
           const int k = k0 + kb * BK;
-          load_op<A_MN, BM>(&ta_hi, &full_bar[s], st, m0, k);
-          load_op<A_MN, BM>(&ta_lo, &full_bar[s], st + A_BYTES, m0, k);
-          load_op<B_MN, BN>(&tb_hi, &full_bar[s], st + 2 * A_BYTES, n0, k);
-          load_op<B_MN, BN>(&tb_lo, &full_bar[s], st + 2 * A_BYTES + B_BYTES, n0, k);
+          load_op<A_MN, PAIR>(&ta_hi, &full_bar[s], st, m0, k);
+          load_op<A_MN, PAIR>(&ta_lo, &full_bar[s], st + A_BYTES, m0, k);
+          load_op<B_MN, PAIR>(&tb_hi, &full_bar[s], st + 2 * A_BYTES, n0, k);
+          load_op<B_MN, PAIR>(&tb_lo, &full_bar[s], st + 2 * A_BYTES + C::B_BYTES, n0, k);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_tf32(A_MN, B_MN);
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_tf32(A_MN, B_MN, BM * PAIR);
       uint32_t it = 0, local = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+      for (int t = slot; t < tiles; t += nslots, ++local) {
         const uint32_t a = local & 1u;
-        if (local >= 2) mbar_wait(&tempty_bar[a], ((local >> 1) & 1u) ^ 1u);  // epilogue drained this slot
+        if (local >= 2) mbar_wait(&tempty_bar[a], ((local >> 1) & 1u) ^ 1u);  // epilogues drained this slot
         tc_fence_after();
         const uint32_t acc_tmem = tmem + a * TMEM_COLS;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
           mbar_wait(&full_bar[s], ph);
           tc_fence_after();
-          const uint32_t st = su32(smem + s * STAGE_BYTES);
-          const uint32_t a_hi = st, a_lo = st + A_BYTES, b_hi = st + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
+          const uint32_t st = su32(smem + s * C::STAGE_BYTES);
+          const uint32_t a_hi = st, a_lo = st + A_BYTES, b_hi = st + 2 * A_BYTES, b_lo = b_hi + C::B_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
+            if (ep.probe & 2u) break;
             const uint32_t accum = (kb > 0 || kk > 0) ? 1u : 0u;
-            mma_tf32(acc_tmem, op_desc<A_MN>(a_hi, kk, ep), op_desc<B_MN>(b_lo, kk, ep), idesc, accum);
-            mma_tf32(acc_tmem, op_desc<A_MN>(a_lo, kk, ep), op_desc<B_MN>(b_hi, kk, ep), idesc, 1u);
-            mma_tf32(acc_tmem, op_desc<A_MN>(a_hi, kk, ep), op_desc<B_MN>(b_hi, kk, ep), idesc, 1u);
+            const uint64_t dah = op_desc<A_MN>(a_hi, kk, ep), dal = op_desc<A_MN>(a_lo, kk, ep);
+            const uint64_t dbh = op_desc<B_MN>(b_hi, kk, ep), dbl = op_desc<B_MN>(b_lo, kk, ep);
+            if (PAIR == 2) {
+              mma_tf32_pair(acc_tmem, dah, dbl, idesc, accum);
+              mma_tf32_pair(acc_tmem, dal, dbh, idesc, 1u);
+              mma_tf32_pair(acc_tmem, dah, dbh, idesc, 1u);
+            } else {
+              mma_tf32(acc_tmem, dah, dbl, idesc, accum);
+              mma_tf32(acc_tmem, dal, dbh, idesc, 1u);
+              mma_tf32(acc_tmem, dah, dbh, idesc, 1u);
+            }
           }
-          mma_commit(&empty_bar[s]);  // stage s is free once these MMAs have read it
+          if (PAIR == 2) mma_commit_pair(&empty_bar[s]);  // stage s is free (in both CTAs) once these MMAs read it
+          else mma_commit(&empty_bar[s]);
         }
-        mma_commit(&tfull_bar[a]);  // accumulator slot a holds the finished tile
+        if (PAIR == 2) mma_commit_pair(&tfull_bar[a]);  // accumulator slot a holds the finished tile
+        else mma_commit(&tfull_bar[a]);
       }
     }
   } else {
-    // epilogue warps 2..5 -> TMEM lane quadrant warp % 4
+    // epilogue warps 2..5 -> TMEM lane quadrant warp % 4 (this CTA's 128 rows of the tile)
     const int q = warp & 3;
     uint32_t local = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+    for (int t = slot; t < tiles; t += nslots, ++local) {
       const int z = t / (mt * nt), r = t % (mt * nt);
-      const int m0 = (r % mt) * BM, n0 = (r / mt) * BN;
+      const int m0 = (r % mt) * BM * PAIR + static_cast<int>(rank) * BM, n0 = (r / mt) * BN;
       const uint32_t a = local & 1u;
-      mbar_wait(&tfull_bar[a], (local >> 1) & 1u);
-      tc_fence_after();
-      const int row = m0 + q * 32 + lane;
       EpiParams e = ep;
       int mode = epi;
       if (splits > 1) {
         mode = kRaw;
         e.partial = ep.partial + static_cast<int64_t>(z) * ep.M * ep.N;
       }
+      // TMEM gives lane = row; the chunk goes through a swizzled 4 KB smem tile (16 B chunk j of row r at
+      // j ^ (r & 7): conflict-free both ways) so each global access of the warp covers 4 whole 128 B rows.
+      float4* stg = reinterpret_cast<float4*>(smem + STAGE_RING_BYTES + q * EPI_STAGE_BYTES);
+      const int ch = lane & 7;
+      float4 aux[8];  // bias / mask operands of the current chunk, prefetched one chunk ahead
+#pragma unroll
+      for (int i = 0; i < 8; ++i) aux[i] = epi_aux(e, mode, m0 + q * 32 + 4 * i + (lane >> 3), n0 + ch * 4);
+      mbar_wait(&tfull_bar[a], (local >> 1) & 1u);
+      tc_fence_after();
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t rr[32];
@@ -315,47 +408,63 @@ __global__ void __launch_bounds__(THREADS, 1)
               "=r"(rr[22]), "=r"(rr[23]), "=r"(rr[24]), "=r"(rr[25]), "=r"(rr[26]), "=r"(rr[27]), "=r"(rr[28]),
               "=r"(rr[29]), "=r"(rr[30]), "=r"(rr[31])
             : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        float v[32];
+        float4 nxt[8];
+        const int cn = c + 32 < BN ? c + 32 : c;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(rr[i]);
-        epi_store(e, mode, row, n0 + c, v);
+        for (int i = 0; i < 8; ++i) nxt[i] = epi_aux(e, mode, m0 + q * 32 + 4 * i + (lane >> 3), n0 + cn + ch * 4);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (ep.probe & 1u) continue;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          stg[lane * 8 + (j ^ (lane & 7))] = make_float4(__uint_as_float(rr[4 * j]), __uint_as_float(rr[4 * j + 1]),
+                                                         __uint_as_float(rr[4 * j + 2]), __uint_as_float(rr[4 * j + 3]));
+        __syncwarp();
+        const int col = n0 + c + ch * 4;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int rw = 4 * i + (lane >> 3);
+          epi_vec4(e, mode, m0 + q * 32 + rw, col, stg[rw * 8 + (ch ^ (rw & 7))], aux[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) aux[i] = nxt[i];
+        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty_bar[a])) : "memory");
+      if (lane == 0) {
+        const uint32_t bar = PAIR == 2 ? (su32(&tempty_bar[a]) & kPeerMask) : su32(&tempty_bar[a]);
+        asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+      }
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR == 2) cluster_sync_all();  // both CTAs are done with the pair's TMEM and barriers
+  else __syncthreads();
   tc_fence_after();
   if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TMEM_COLS) : "memory");
+    if (PAIR == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TMEM_COLS) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TMEM_COLS) : "memory");
   }
 }
 
 // Split-K: sum the partial tiles in ascending split order, then the epilogue (deterministic, no atomics).
 __global__ void splitk_reduce_kernel(int splits, int epi, EpiParams ep) {
-  const int64_t total = static_cast<int64_t>(ep.M) * ep.N / 32;
+  const int64_t total = static_cast<int64_t>(ep.M) * ep.N / 4;
   for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < total;
        g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t e0 = g * 32;
+    const int64_t e0 = g * 4;
     const int row = static_cast<int>(e0 / ep.N), col = static_cast<int>(e0 % ep.N);
-    float v[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = 0.f;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s = 0; s < splits; ++s) {
-      const float* p = ep.partial + static_cast<int64_t>(s) * ep.M * ep.N + e0;
-#pragma unroll
-      for (int i = 0; i < 32; i += 4) {
-        float4 q = *reinterpret_cast<const float4*>(p + i);
-        v[i] += q.x;
-        v[i + 1] += q.y;
-        v[i + 2] += q.z;
-        v[i + 3] += q.w;
-      }
+      const float4 q = *reinterpret_cast<const float4*>(ep.partial + static_cast<int64_t>(s) * ep.M * ep.N + e0);
+      v.x += q.x;
+      v.y += q.y;
+      v.z += q.z;
+      v.w += q.w;
     }
-    epi_store(ep, epi, row, col, v);
+    epi_vec4(ep, epi, row, col, v, epi_aux(ep, epi, row, col));
   }
 }
 
@@ -504,11 +613,20 @@ CUtensorMap make_map(const OpView& v, int tile_rows) {
 struct GemmPlan {
   CUtensorMap a_hi, a_lo, b_hi, b_lo;
   bool a_mn = false, b_mn = false;
-  int M = 0, N = 0, K = 0, splits = 1, epi = 0;
+  int M = 0, N = 0, K = 0, splits = 1, epi = 0, pair = 1;
   EpiParams ep{};
 };
 
-template <bool A_MN, bool B_MN>
+int sm_count() {
+  static int sms = [] {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, 0);
+    return v > 0 ? v : 148;
+  }();
+  return sms;
+}
+
+template <bool A_MN, bool B_MN, int PAIR>
 void launch_variant(const GemmPlan& p, cudaStream_t st) {
   // the dynamic-smem opt-in is per device: remember which devices this instantiation was configured on
   static std::mutex mu;
@@ -518,44 +636,60 @@ void launch_variant(const GemmPlan& p, cudaStream_t st) {
   {
     std::lock_guard<std::mutex> lk(mu);
     if (!(configured >> dev & 1ull)) {
-      LSGD_CUDA(cudaFuncSetAttribute(gemm_tf32x3_kernel<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     SMEM_BYTES));
+      LSGD_CUDA(cudaFuncSetAttribute(gemm_tf32x3_kernel<A_MN, B_MN, PAIR>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
       configured |= 1ull << dev;
     }
   }
-  static int sms = [] {
-    int v = 0;
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, 0);
-    return v > 0 ? v : 148;
-  }();
-  const int tiles = (p.N / BN) * (p.M / BM) * p.splits;
-  const int grid = tiles < sms ? tiles : sms;
-  gemm_tf32x3_kernel<A_MN, B_MN><<<grid, THREADS, SMEM_BYTES, st>>>(p.a_hi, p.a_lo, p.b_hi, p.b_lo, p.epi,
-                                                                    p.K / p.splits, p.splits, p.ep);
+  const int tiles = (p.N / BN) * (p.M / (BM * PAIR)) * p.splits;
+  const int slots = sm_count() / PAIR;
+  const int grid = (tiles < slots ? tiles : slots) * PAIR;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = PAIR;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  LSGD_CUDA(cudaLaunchKernelEx(&cfg, gemm_tf32x3_kernel<A_MN, B_MN, PAIR>, p.a_hi, p.a_lo, p.b_hi, p.b_lo, p.epi,
+                               p.K / p.splits, p.splits, p.ep));
+}
+
+template <int PAIR>
+void launch_pair(const GemmPlan& p, cudaStream_t st) {
+  if (!p.a_mn && !p.b_mn) launch_variant<false, false, PAIR>(p, st);
+  else if (!p.a_mn && p.b_mn) launch_variant<false, true, PAIR>(p, st);
+  else if (p.a_mn && p.b_mn) launch_variant<true, true, PAIR>(p, st);
+  else launch_variant<true, false, PAIR>(p, st);
 }
 
 void run_plan(const GemmPlan& p, cudaStream_t st, LaunchCounter& lc) {
-  if (!p.a_mn && !p.b_mn) launch_variant<false, false>(p, st);
-  else if (!p.a_mn && p.b_mn) launch_variant<false, true>(p, st);
-  else if (p.a_mn && p.b_mn) launch_variant<true, true>(p, st);
-  else launch_variant<true, false>(p, st);
+  if (p.pair == 2) launch_pair<2>(p, st);
+  else launch_pair<1>(p, st);
   ++lc.n;
   LSGD_CUDA(cudaGetLastError());
   static const bool probe_sync = std::getenv("LSGD_TC_SYNC") != nullptr;
   if (probe_sync) LSGD_CUDA(cudaStreamSynchronize(st));
   if (p.splits > 1) {
-    int64_t work = static_cast<int64_t>(p.M) * p.N / 32;
+    int64_t work = static_cast<int64_t>(p.M) * p.N / 4;
     int grid = static_cast<int>(std::min<int64_t>((work + 255) / 256, 148 * 8));
     splitk_reduce_kernel<<<grid, 256, 0, st>>>(p.splits, p.epi, p.ep);
     ++lc.n;
-  LSGD_CUDA(cudaGetLastError());
+    LSGD_CUDA(cudaGetLastError());
   }
 }
 
-int choose_splits(int M, int N, int K) {
-  int tiles = (M / BM) * (N / BN);
+// Split K (ordered partial reduction) only when the tiles alone leave most SMs idle.
+int choose_splits(int M, int N, int K, int pair) {
+  const int tiles = (M / (BM * pair)) * (N / BN);
+  const int slots = 160 / pair;
   int s = 1;
-  while (tiles * s * 2 <= 160 && K % (BK * s * 2) == 0 && K / (s * 2) >= 4 * BK) s *= 2;
+  while (tiles * s * 2 <= slots && K % (BK * s * 2) == 0 && K / (s * 2) >= 4 * BK) s *= 2;
   return s;
 }
 
@@ -570,14 +704,17 @@ GemmPlan make_plan(const OpView& a_hi, const float* a_lo, const OpView& b_hi, co
   check<Error>(a_hi.k == b_hi.k, "gemm: K mismatch");
   check<Error>(p.M % BM == 0 && p.N % BN == 0 && p.K % BK == 0, "gemm: shape ", p.M, "x", p.N, "x", p.K,
                " is not a multiple of the 128x256x32 tile");
+  // CTA pairs whenever the M extent allows 256-row tiles (LSGD_TC_PAIR=0 forces single CTAs: tuning only)
+  static const bool no_pair = std::getenv("LSGD_TC_PAIR") && std::atoi(std::getenv("LSGD_TC_PAIR")) == 0;
+  p.pair = (!no_pair && p.M % (2 * BM) == 0) ? 2 : 1;
   p.a_hi = make_map(a_hi, BM);
   OpView al = a_hi;
   al.ptr = a_lo;
   p.a_lo = make_map(al, BM);
-  p.b_hi = make_map(b_hi, BN);
+  p.b_hi = make_map(b_hi, BN / p.pair);
   OpView bl = b_hi;
   bl.ptr = b_lo;
-  p.b_lo = make_map(bl, BN);
+  p.b_lo = make_map(bl, BN / p.pair);
   p.epi = epi;
   p.ep = ep;
   const MnGeometry& g = mn_geometry();
@@ -586,12 +723,14 @@ GemmPlan make_plan(const OpView& a_hi, const float* a_lo, const OpView& b_hi, co
   p.ep.mn_layout = g.layout;
   static const bool no_prefetch = std::getenv("LSGD_TC_NOPREFETCH") != nullptr;  // bring-up probe only
   p.ep.prefetch = no_prefetch ? 0u : 1u;
+  static const uint32_t probe = std::getenv("LSGD_TC_PROBE") ? std::atoi(std::getenv("LSGD_TC_PROBE")) : 0;
+  p.ep.probe = probe;
   int ex = 0;
   p.ep.div_pow2 = (ep.div > 0.f && std::frexp(ep.div, &ex) == 0.5f) ? 1 : 0;
   p.ep.div_inv = p.ep.div_pow2 ? 1.0f / ep.div : 0.f;
   p.ep.M = p.M;
   p.ep.N = p.N;
-  p.splits = std::getenv("LSGD_TC_NOSPLIT") ? 1 : choose_splits(p.M, p.N, p.K);
+  p.splits = std::getenv("LSGD_TC_NOSPLIT") ? 1 : choose_splits(p.M, p.N, p.K, p.pair);
   if (static_cast<size_t>(p.splits) * p.M * p.N > partial_elems) p.splits = 1;
   p.ep.partial = partial;
   return p;
@@ -724,9 +863,11 @@ void tc_split_weights(TcWorkspace& ws, const Layout& L, const float* w, cudaStre
   split(w, L.n_params, ws.w_hi, ws.w_lo, st, lc);
 }
 
-void tc_forward_layer(TcWorkspace& ws, const Layout& L, int k, const float* w, const float* x, cudaStream_t st,
-                      LaunchCounter& lc) {
-  if (k == 0) split(x, static_cast<int64_t>(ws.batch) * L.in(0), ws.x_hi, ws.x_lo, st, lc);
+void tc_split_input(TcWorkspace& ws, const Layout& L, const float* x, cudaStream_t st, LaunchCounter& lc) {
+  split(x, static_cast<int64_t>(ws.batch) * L.in(0), ws.x_hi, ws.x_lo, st, lc);
+}
+
+void tc_forward_layer(TcWorkspace& ws, const Layout& L, int k, const float* w, cudaStream_t st, LaunchCounter& lc) {
   GemmPlan p = ws.layers[static_cast<size_t>(k)]->fwd;
   p.ep.bias = w + L.b_off[static_cast<size_t>(k)];
   run_plan(p, st, lc);
@@ -864,7 +1005,8 @@ void tc_debug_step(const std::vector<int32_t>& layers, int batch, const float* w
   LaunchCounter lc;
   cudaStream_t st = 0;
   tc_split_weights(ws, L, w, st, lc);
-  for (int k = 0; k < L.depth(); ++k) tc_forward_layer(ws, L, k, w, x, st, lc);
+  tc_split_input(ws, L, x, st, lc);
+  for (int k = 0; k < L.depth(); ++k) tc_forward_layer(ws, L, k, w, st, lc);
   tc_head(ws, L, y, sl, loss, st, lc);
   LSGD_CUDA(cudaDeviceSynchronize());
   int64_t off = 0;

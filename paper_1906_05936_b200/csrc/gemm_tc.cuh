@@ -41,9 +41,10 @@ void tc_alloc(TcWorkspace& ws, const Layout& L, int batch, int n_features);
 void tc_free(TcWorkspace& ws);
 // w -> (w_hi, w_lo) for the whole parameter vector (initial parameters; afterwards the fused update writes it).
 void tc_split_weights(TcWorkspace& ws, const Layout& L, const float* w, cudaStream_t st, LaunchCounter& lc);
-// Forward layer k (k = 0 first splits the gathered batch x): act_k = ReLU?(in . W_k^T + b_k) and its split.
-void tc_forward_layer(TcWorkspace& ws, const Layout& L, int k, const float* w, const float* x, cudaStream_t st,
-                      LaunchCounter& lc);
+// Gathered batch x -> (x_hi, x_lo), the operand of the first forward GEMM.
+void tc_split_input(TcWorkspace& ws, const Layout& L, const float* x, cudaStream_t st, LaunchCounter& lc);
+// Forward layer k: act_k = ReLU?(in . W_k^T + b_k) and its split.
+void tc_forward_layer(TcWorkspace& ws, const Layout& L, int k, const float* w, cudaStream_t st, LaunchCounter& lc);
 // Softmax-CE head: delta of the top layer (+ split), per-sample losses, mean loss -> *loss_out.
 void tc_head(TcWorkspace& ws, const Layout& L, const int32_t* y, float* sample_loss, float* loss_out, cudaStream_t st,
              LaunchCounter& lc);

@@ -14,7 +14,9 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <cstdio>
 #include <map>
+#include <tuple>
 #include <mutex>
 
 #include "engine.hpp"
@@ -126,7 +128,9 @@ class RankImpl final : public Rank {
     if (split_) LSGD_CUDA(cudaStreamCreateWithFlags(&upd_, cudaStreamNonBlocking));
     else upd_ = main_;
     for (int b = 0; b < kMaxBuckets; ++b) LSGD_CUDA(cudaEventCreateWithFlags(&ev_upd_[b], cudaEventDisableTiming));
+    for (int b = 0; b < kMaxBuckets; ++b) LSGD_CUDA(cudaEventCreateWithFlags(&ev_dx_[b], cudaEventDisableTiming));
     for (int b = 0; b < kMaxBuckets; ++b) LSGD_CUDA(cudaEventCreateWithFlags(&ev_bucket_[b], cudaEventDisableTiming));
+    LSGD_CUDA(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming));
     void* to = nullptr;
     LSGD_CUDA(cudaHostAlloc(&to, sizeof(int), cudaHostAllocMapped));
     timed_out_host_ = static_cast<volatile int*>(to);
@@ -169,6 +173,8 @@ class RankImpl final : public Rank {
             cudaEventDestroy(pe.ev[p][1]);
           }
     for (auto& w : ws_) free_worker(w);
+    for (T* p : own_x_) cudaFree(p);
+    for (int32_t* p : own_y_) cudaFree(p);
     for (char* p : ipc_opened_) cudaIpcCloseMemHandle(p);
     if (slice_comm_) ncclCommDestroy(slice_comm_);
     if (flat_comm_) ncclCommDestroy(flat_comm_);
@@ -190,6 +196,18 @@ class RankImpl final : public Rank {
       cudaStreamDestroy(upd_);
     }
     for (int b = 0; b < kMaxBuckets; ++b) cudaEventDestroy(ev_upd_[b]);
+    for (int b = 0; b < kMaxBuckets; ++b) cudaEventDestroy(ev_dx_[b]);
+    cudaEventDestroy(join_ev_);
+    if (base_ev_) cudaEventDestroy(base_ev_);
+    if (io_) {
+      cudaStreamDestroy(io_);
+      for (int i = 0; i < 2; ++i) {
+        cudaFree(rows_xbuf_[i]);
+        cudaFree(rows_ybuf_[i]);
+        cudaEventDestroy(ev_rows_h2d_[i]);
+        cudaEventDestroy(ev_rows_free_[i]);
+      }
+    }
     cudaStreamDestroy(main_);
   }
 
@@ -354,6 +372,15 @@ class RankImpl final : public Rank {
     }
   }
 
+  int loss_async(void* host_pinned) override {
+    LSGD_CUDA(cudaSetDevice(dev_));
+    check<Error>(applied_ > 0, "no round has been applied yet");
+    cudaStream_t st = (alg_ == LSGD_B200_LSGD && split_) ? upd_ : main_;  // the stream the round's update ran on
+    Timed tm(this, "d2h", st);
+    LSGD_CUDA(cudaMemcpyAsync(host_pinned, ws_[0].loss_hist + (applied_ - 1) % kLossCap, sizeof(T),
+                              cudaMemcpyDeviceToHost, st));
+    return static_cast<int>(sizeof(T));
+  }
   double last_loss() override {
     synchronize();
     if (applied_ == 0) return 0.0;
@@ -362,12 +389,22 @@ class RankImpl final : public Rank {
     return static_cast<double>(v);
   }
 
+  void join() override {
+    LSGD_CUDA(cudaSetDevice(dev_));
+    for (cudaStream_t st : {comm_, upd_, io_}) {
+      if (st == nullptr || st == main_) continue;
+      LSGD_CUDA(cudaEventRecord(join_ev_, st));
+      LSGD_CUDA(cudaStreamWaitEvent(main_, join_ev_, 0));
+    }
+  }
   int64_t launches() const override { return lc_.n; }
   void* main_stream() override { return main_; }
   void set_timing(bool on) override {
     timing_ = on;
     if (on) {
       LSGD_CUDA(cudaSetDevice(dev_));
+      if (base_ev_ == nullptr) LSGD_CUDA(cudaEventCreate(&base_ev_));
+      LSGD_CUDA(cudaEventRecord(base_ev_, main_));
       for (auto& kv : timers_)
         for (auto& pr : kv.second) {
           cudaEventDestroy(pr.first);
@@ -375,6 +412,25 @@ class RankImpl final : public Rank {
         }
       timers_.clear();
     }
+  }
+  std::string timeline() override {
+    synchronize();
+    std::vector<std::tuple<float, float, std::string>> rows;
+    for (auto& kv : timers_)
+      for (auto& pr : kv.second) {
+        float a = 0, b = 0;
+        LSGD_CUDA(cudaEventElapsedTime(&a, base_ev_, pr.first));
+        LSGD_CUDA(cudaEventElapsedTime(&b, base_ev_, pr.second));
+        rows.emplace_back(a, b, kv.first);
+      }
+    std::sort(rows.begin(), rows.end());
+    std::string out;
+    char line[128];
+    for (auto& r : rows) {
+      std::snprintf(line, sizeof(line), "%s\t%.4f\t%.4f\n", std::get<2>(r).c_str(), std::get<0>(r), std::get<1>(r));
+      out += line;
+    }
+    return out;
   }
   void kernel_time(const std::string& fam, double* avg_ms, int64_t* count) override {
     synchronize();
@@ -496,6 +552,8 @@ class RankImpl final : public Rank {
         LSGD_CUDA(cudaMalloc(&w.d1, sizeof(T) * static_cast<size_t>(B_) * wide));
       }
     }
+    own_x_.push_back(w.x);
+    own_y_.push_back(w.y);
     ws_.push_back(std::move(w));
     peer_base_[static_cast<size_t>(wid)] = ws_.back().blk;
   }
@@ -505,8 +563,6 @@ class RankImpl final : public Rank {
     cudaFree(w.w);
     if (w.v) cudaFree(w.v);
     cudaFree(w.loss_hist);
-    if (w.x) cudaFree(w.x);
-    if (w.y) cudaFree(w.y);
     if (w.idx) cudaFree(w.idx);
     for (T* a : w.act) cudaFree(a);
     if (w.d0) cudaFree(w.d0);
@@ -608,16 +664,40 @@ class RankImpl final : public Rank {
   void io(int64_t t, const int32_t* given, bool shard_only) {
     if (rows_x_) {  // caller-supplied host rows: the H2D copy is the io
       const int d = spec_.c.n_features;
-      for (size_t i = 0; i < ws_.size(); ++i) {
+      const size_t nw = ws_.size();
+      if (io_ == nullptr) {
+        LSGD_CUDA(cudaStreamCreateWithFlags(&io_, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+          LSGD_CUDA(cudaMalloc(&rows_xbuf_[i], sizeof(T) * nw * B_ * d));
+          LSGD_CUDA(cudaMalloc(&rows_ybuf_[i], sizeof(int32_t) * nw * B_));
+          LSGD_CUDA(cudaEventCreateWithFlags(&ev_rows_h2d_[i], cudaEventDisableTiming));
+          LSGD_CUDA(cudaEventCreateWithFlags(&ev_rows_free_[i], cudaEventDisableTiming));
+        }
+      }
+      const int slot = static_cast<int>(t & 1);
+      if (rows_used_[slot]) LSGD_CUDA(cudaStreamWaitEvent(io_, ev_rows_free_[slot], 0));
+      {
+        Timed tm(this, "h2d", io_);
+        LSGD_CUDA(cudaMemcpyAsync(rows_xbuf_[slot], rows_x_, sizeof(T) * nw * B_ * d, cudaMemcpyHostToDevice, io_));
+        LSGD_CUDA(cudaMemcpyAsync(rows_ybuf_[slot], rows_y_, sizeof(int32_t) * nw * B_, cudaMemcpyHostToDevice, io_));
+      }
+      LSGD_CUDA(cudaEventRecord(ev_rows_h2d_[slot], io_));
+      rows_used_[slot] = true;
+      rows_slot_ = slot;
+      for (size_t i = 0; i < nw; ++i) {
         Worker& w = ws_[i];
         phase_mark(i, t, 0, 0, main_);
         launch_sleep(spec_.c.io_delay_s, main_, lc_);
-        LSGD_CUDA(cudaMemcpyAsync(w.x, rows_x_ + i * static_cast<size_t>(B_) * d, sizeof(T) * B_ * d,
-                                  cudaMemcpyHostToDevice, main_));
-        LSGD_CUDA(cudaMemcpyAsync(w.y, rows_y_ + i * B_, sizeof(int32_t) * B_, cudaMemcpyHostToDevice, main_));
+        if (i == 0) LSGD_CUDA(cudaStreamWaitEvent(main_, ev_rows_h2d_[slot], 0));
+        w.x = rows_xbuf_[slot] + i * static_cast<size_t>(B_) * d;
+        w.y = rows_ybuf_[slot] + i * static_cast<size_t>(B_);
         phase_mark(i, t, 0, 1, main_);
       }
       return;
+    }
+    for (size_t i = 0; i < ws_.size(); ++i) {  // gathered rows land in the worker's own batch buffers
+      ws_[i].x = own_x_[i];
+      ws_[i].y = own_y_[i];
     }
     const int slot = static_cast<int>(t % kRing);
     LSGD_CUDA(cudaEventSynchronize(ring_ev_[slot]));  // the copy that last used this slot has completed
@@ -656,12 +736,16 @@ class RankImpl final : public Rank {
 
   void forward_layer(Worker& w, int k) {
     if (synth_) return;
-    Timed tm(this, "gemm", main_);
     if (use_tc_) {
-      tc_forward_layer(w.tc, L_, k, reinterpret_cast<const float*>(w.w), reinterpret_cast<const float*>(w.x), main_,
-                       lc_);
+      if (k == 0) {
+        Timed ts(this, "split", main_);
+        tc_split_input(w.tc, L_, reinterpret_cast<const float*>(w.x), main_, lc_);
+      }
+      Timed tm(this, "gemm", main_);
+      tc_forward_layer(w.tc, L_, k, reinterpret_cast<const float*>(w.w), main_, lc_);
       return;
     }
+    Timed tm(this, "gemm", main_);
     const int ni = L_.in(k), no = L_.out(k);
     const T* in = k == 0 ? w.x : w.act[static_cast<size_t>(k - 1)];
     const T* Wk = w.w + L_.w_off[static_cast<size_t>(k)];
@@ -673,6 +757,7 @@ class RankImpl final : public Rank {
   void head(Worker& w) {
     if (synth_) return;
     T* loss_out = w.payload + geo_.loss_at;
+    Timed tm(this, "head", main_);
     if (use_tc_) {
       tc_head(w.tc, L_, w.y, reinterpret_cast<float*>(w.sample_loss), reinterpret_cast<float*>(loss_out), main_, lc_);
       return;
@@ -690,12 +775,18 @@ class RankImpl final : public Rank {
     const int ni = L_.in(k), no = L_.out(k);
     T* gW = w.payload + bk.poff;
     T* gb = gW + static_cast<int64_t>(bk.rows) * ni;
-    Timed tm(this, "gemm", main_);
     if (use_tc_) {
-      tc_backward_dw(w.tc, L_, k, bk.row0, bk.rows, reinterpret_cast<float*>(gW), main_, lc_);
-      if (bk.bias) tc_backward_bias(w.tc, L_, k, reinterpret_cast<float*>(gb), main_, lc_);
+      {
+        Timed tm(this, "gemm", main_);
+        tc_backward_dw(w.tc, L_, k, bk.row0, bk.rows, reinterpret_cast<float*>(gW), main_, lc_);
+      }
+      if (bk.bias) {
+        Timed tb(this, "bias", main_);
+        tc_backward_bias(w.tc, L_, k, reinterpret_cast<float*>(gb), main_, lc_);
+      }
       return;
     }
+    Timed tm(this, "gemm", main_);
     const T* dcur = delta_buf(w, k);
     const T* aprev = k == 0 ? w.x : w.act[static_cast<size_t>(k - 1)];
     launch_gemm_simt<T>(kEpiWeightGrad, exact_, bk.rows, ni, B_, dcur + bk.row0, 1, no, aprev, ni, 1, gW, ni, nullptr,
@@ -831,27 +922,19 @@ class RankImpl final : public Rank {
     if (!synth_) io(t, given, shard_only);
     else launch_sleep(spec_.c.io_delay_s, main_, lc_);
 
-    // postponed update of round t-1, bucket by bucket, each finished right before the forward of its layer.
-    // One worker per rank: the updates run on their own stream, so the next layer's update (waiting for its averaged
-    // gradient, then streaming w/v through HBM) overlaps the forward GEMM of the current layer.
-    const bool postponed = alg_ == LSGD_B200_LSGD && t >= 1;
-    if (postponed && split_) {
-      Worker& w = ws_[0];
-      current_phase() = "broadcast";
-      for (int b = 0; b < NB; ++b) {
-        if (reduce_folded()) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_bucket_[b], 0));  // payload b of round t-1
-        apply_bucket(w, b, t - 1, upd_);
-        LSGD_CUDA(cudaEventRecord(ev_upd_[b], upd_));
-      }
-      after_update(w, t - 1, upd_);
-    }
+    // Update of round t-1 (the postponed update of executors.cpp:210-229). With one worker per rank it was already
+    // issued during step t-1 on the update stream, bucket by bucket as soon as (a) the bucket's averaged gradient
+    // had arrived and (b) the backward of step t-1 no longer read W_k (after dX_k): the forward of layer k only
+    // waits for its buckets' events. Emulated ranks (several workers on one stream) apply it here, in order.
+    const bool eager = alg_ == LSGD_B200_LSGD && split_;
+    const bool postponed = alg_ == LSGD_B200_LSGD && t >= 1 && !split_;
     const bool exchange = !flat_nccl() && !reduce_folded() && alg_ != LSGD_B200_SEQUENTIAL;
     for (auto& w : ws_) {
       current_phase() = "compute";
       phase_mark(widx(w), t, 1, 0, main_);
       for (int k = 0; k < D; ++k) {
         for (int b : LB[static_cast<size_t>(k)]) {
-          if (postponed && split_) {
+          if (eager && t >= 1) {
             LSGD_CUDA(cudaStreamWaitEvent(main_, ev_upd_[b], 0));
           } else if (postponed) {
             current_phase() = "broadcast";
@@ -861,22 +944,36 @@ class RankImpl final : public Rank {
         }
         forward_layer(w, k);
       }
-      if (postponed && !split_) after_update(w, t - 1, main_);
+      if (postponed) after_update(w, t - 1, main_);
       head(w);
       for (int k = D - 1; k >= 0; --k) {
-        if (!synth_) {
-          for (int b : LB[static_cast<size_t>(k)]) {
-            backward_bucket(w, b);  // row block of dW_k (+ db_k): ready for the exchange right away
-            if (exchange) signal(w, kFlagGrad, b, static_cast<unsigned long long>(t + 1), main_);
-            if (split_) LSGD_CUDA(cudaEventRecord(ev_bucket_[b], main_));
+        // dX_k first: after it W_k is no longer read by this step, so each row block's update (eager) can follow
+        // its dW block immediately, overlapping the remaining weight-gradient GEMMs
+        if (!synth_) backward_input(w, k);
+        if (eager) {
+          LSGD_CUDA(cudaEventRecord(ev_dx_[k], main_));
+          LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_dx_[k], 0));
+        }
+        for (int b : LB[static_cast<size_t>(k)]) {
+          if (!synth_) backward_bucket(w, b);  // row block of dW_k (+ db_k): ready for the exchange right away
+          if (exchange) signal(w, kFlagGrad, b, static_cast<unsigned long long>(t + 1), main_);
+          if (split_) LSGD_CUDA(cudaEventRecord(ev_bucket_[b], main_));
+          if (eager) {
+            current_phase() = "broadcast";
+            if (reduce_folded()) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_bucket_[b], 0));
+            apply_bucket(w, b, t, upd_);
+            LSGD_CUDA(cudaEventRecord(ev_upd_[b], upd_));
+            current_phase() = "compute";
           }
-          backward_input(w, k);
-        } else {
-          if (exchange) signal(w, kFlagGrad, 0, static_cast<unsigned long long>(t + 1), main_);
-          if (split_) LSGD_CUDA(cudaEventRecord(ev_bucket_[0], main_));
         }
       }
+      if (eager) after_update(w, t, upd_);
       phase_mark(widx(w), t, 1, 1, main_);
+    }
+    if (eager) ++applied_;
+    if (rows_slot_ >= 0) {  // this step's staged host rows are no longer read
+      LSGD_CUDA(cudaEventRecord(ev_rows_free_[rows_slot_], main_));
+      rows_slot_ = -1;
     }
     if (postponed) ++applied_;
 
@@ -953,6 +1050,19 @@ class RankImpl final : public Rank {
   cudaStream_t main_ = nullptr, comm_ = nullptr;
   cudaEvent_t ev_bucket_[kMaxBuckets] = {};
   cudaEvent_t ev_upd_[kMaxBuckets] = {};
+  cudaEvent_t ev_dx_[kMaxBuckets] = {};
+  cudaEvent_t base_ev_ = nullptr;  // timeline origin (set_timing)
+  cudaEvent_t join_ev_ = nullptr;
+  // caller-supplied host rows (step_rows): H2D on io_ into a double-buffered staging pair, overlapping the
+  // previous step; ev_rows_free_[s] = the step that last read slot s has finished with it
+  cudaStream_t io_ = nullptr;
+  T* rows_xbuf_[2] = {nullptr, nullptr};
+  int32_t* rows_ybuf_[2] = {nullptr, nullptr};
+  cudaEvent_t ev_rows_h2d_[2] = {}, ev_rows_free_[2] = {};
+  bool rows_used_[2] = {false, false};
+  int rows_slot_ = -1;
+  std::vector<T*> own_x_;
+  std::vector<int32_t*> own_y_;  // per layer: dX_k issued (W_k free for its update)
   cudaStream_t upd_ = nullptr;
   std::vector<char*> peer_base_;
   std::vector<char*> ipc_opened_;

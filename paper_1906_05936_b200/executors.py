@@ -286,6 +286,17 @@ class Rank:
         N.check(N.lib.lsgd_b200_rank_last_loss(self.h, C.byref(v)))
         return v.value
 
+    def join(self) -> None:
+        """Order the rank's stream after all work issued so far on its side streams (no host sync)."""
+        N.check(N.lib.lsgd_b200_rank_join(self.h))
+
+    def loss_async(self, host_pinned_ptr: int) -> int:
+        """Enqueue the D2H copy of the latest applied round's loss into pinned host memory (no host sync);
+        returns the element size in bytes (4 for fp32, 8 for fp64)."""
+        n = C.c_int32()
+        N.check(N.lib.lsgd_b200_rank_loss_async(self.h, C.c_void_p(host_pinned_ptr), C.byref(n)))
+        return n.value
+
     def params(self) -> np.ndarray:
         w = np.zeros(self.cfg.n_params)
         N.check(N.lib.lsgd_b200_rank_get_params(self.h, w.ctypes.data, w.size))

@@ -47,6 +47,22 @@ def test_gemm_majors_fp32_accurate(a_mn, b_mn):
     assert np.abs(got - ref).max() < 1e-3
 
 
+@pytest.mark.parametrize("M", [128, 384, 768])
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 1), (0, 1)])
+def test_gemm_single_cta_and_pair_tiles(M, a_mn, b_mn):
+    """M % 256 != 0 runs single-CTA 128-row tiles; M = 768 runs CTA-pair (cta_group::2) 256-row tiles."""
+    rng = np.random.default_rng(M + 3 * a_mn + b_mn)
+    Nn, K = 768, 272
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((Nn, K)).astype(np.float32)
+    mask = (rng.standard_normal((M, Nn)) > 0).astype(np.float32)
+    ref = A.astype(np.float64) @ B.astype(np.float64).T
+    got = tc_gemm(A, B, a_mn, b_mn, epi=1, div=1.0)
+    assert rel(got, ref) < 3e-6, rel(got, ref)
+    ig = tc_gemm(A, B, a_mn, b_mn, epi=2, mask=mask)
+    assert rel(ig, ref * mask) < 3e-6
+
+
 def test_gemm_epilogues_and_split_k():
     rng = np.random.default_rng(7)
     M, Nn, K = 256, 256, 4096  # few tiles, long K -> split-K with ordered partial reduction
