@@ -34,7 +34,7 @@ METRIC = "samples/sec (LSGD step, weak scaling, B_loc per GPU)"
 UNIT = "samples/s"
 
 
-def workload(name: str, n: int, bloc: int | None, algo: str):
+def workload(name: str, n: int, bloc: int | None, algo: str, glob: str = "ordered"):
     import paper_1906_05936_b200 as lsgd
 
     G = min(2, n) if algo == "lsgd" else 1
@@ -54,7 +54,7 @@ def workload(name: str, n: int, bloc: int | None, algo: str):
         cfg.b200.synthetic_params = 25_600_000
     else:
         raise SystemExit(f"unknown workload {name}")
-    cfg.b200.global_allreduce = "nccl"
+    cfg.b200.global_allreduce = glob
     if algo == "csgd":
         cfg.b200.csgd_nccl = True
     return cfg
@@ -203,7 +203,7 @@ def run_b200_arm(args):
         pg.all_gather_object(out, obj)
         return out
 
-    cfg = workload(args.workload, n, args.bloc, args.algo)
+    cfg = workload(args.workload, n, args.bloc, args.algo, args.global_allreduce)
     t_setup = time.time()
     r = Rank(cfg, rank, local)
     r.connect(allgather(r.export()))
@@ -232,7 +232,8 @@ def run_b200_arm(args):
     launches = r.launches() - l0
     clk = clocks.finish() if clocks else None
     r.timing(False)
-    fams = {f: r.kernel_time(f) for f in ("gemm", "reduce", "global", "broadcast", "update", "gather")}
+    fams = {f: r.kernel_time(f) for f in ("gemm", "scatter", "reduce", "global", "broadcast", "update", "gather",
+                                          "bias", "head", "split")}
     ms_all = allgather(ms)
     ms_max = max(ms_all)
     B = cfg.local_batch
@@ -343,6 +344,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg1", "cfg4"])
     ap.add_argument("--algo", default="lsgd", choices=["lsgd", "csgd"])
+    ap.add_argument("--global-allreduce", default="ordered", choices=["nccl", "ordered"],
+                    help="LSGD inter-group average: NCCL over the slot owners, or the ordered push sum")
     ap.add_argument("--bloc", type=int, default=None)
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")

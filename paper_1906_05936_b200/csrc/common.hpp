@@ -8,6 +8,9 @@
 
 namespace lsgd_b200 {
 
+constexpr int kMaxPeers = 16;  // max workers per group and groups per world (flag fan-in / fan-out)
+
+
 class Error : public std::runtime_error {
  public:
   explicit Error(const std::string& what) : std::runtime_error(what) {}

@@ -31,12 +31,21 @@ struct PeerLayout {
   int64_t s[2] = {0, 0};  // Sg elements each (double-buffered by step parity)
   int64_t gbar = 0;      // Sg elements
   int64_t gfull = 0;     // Ppad elements: the whole averaged gradient, pushed here by the group's slot owners
+  // push exchange (one worker per GPU): stage[m] (Sg each) = member m's sub-slices of this worker's slot, pushed
+  // by m after its weight-gradient GEMMs; gstage[par][g] (Sg each) = group g's slot sum, pushed by g's owner
+  int64_t stage = 0;
+  int64_t gstage[2] = {0, 0};
   int64_t total = 0;
 };
 enum : int { kFlagGrad = 0, kFlagSlice = 1, kFlagBcast = 2 };
 constexpr int kMaxBuckets = 32;
 // flags[kArrived + b * kMaxPeers + j]: round counter of the averaged sub-slice j of bucket b pushed by slot j
 constexpr int kArrived = 3 * kMaxBuckets;
+// flags[kStaged + b * kMaxPeers + m]: member m's sub-slice of bucket b is in this owner's stage[m]
+constexpr int kStaged = kArrived + kMaxBuckets * kMaxPeers;
+// flags[kGsum + b * kMaxPeers + g]: group g's slot sum of bucket b is in this owner's gstage[par][g]
+constexpr int kGsum = kStaged + kMaxBuckets * kMaxPeers;
+constexpr int kFlagWords = kGsum + kMaxBuckets * kMaxPeers;
 
 // Gradient buckets: one per layer (that layer's [W_k | b_k] block, contiguous in the reference's parameter
 // layout, mlp.hpp:14-18), the loss slot riding the last layer's bucket. Each bucket is split into k sub-slices of

@@ -64,7 +64,19 @@ struct EpiParams {
   int div_pow2;                        // div is a power of two: multiply by the exact reciprocal
   float div_inv;
   uint32_t probe;  // bring-up/tuning only (LSGD_TC_PROBE): 1 skip epilogue stores, 2 skip MMAs, 4 skip TMA loads
+  BucketScatter scat;  // weight-gradient output routed to the sub-slice owners (n = 0: plain ep.out)
+  int fuse_upd;        // weight gradient: apply the update (upd) instead of storing the gradient
+  FusedUpdate upd;
 };
+
+
+
+// Destination of bucket-local element e (a float4 never straddles sub-slices: S is a multiple of 64).
+__device__ __forceinline__ float* scatter_at(const BucketScatter& sc, int64_t e) {
+  int j = 0;
+  while (j + 1 < sc.n && e >= (j + 1) * sc.S) ++j;
+  return sc.dst[j] + (e - j * sc.S);
+}
 
 // ------------------------------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -206,20 +218,58 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float(r);
 }
 
+// K8 on 4 consecutive parameters (same operations as update_kernel<float, false>), w4/v4 already loaded: stores
+// w, v and the TF32 split; returns true if a result is non-finite.
+__device__ __forceinline__ bool fused_update4(const FusedUpdate& u, int64_t at, const float* g, float4 w4, float4 v4) {
+  float w[4] = {w4.x, w4.y, w4.z, w4.w}, v[4] = {v4.x, v4.y, v4.z, v4.w};
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float d = g[i];
+    if (u.add_zero) d = __fadd_rn(d, 0.f);
+    if (u.post_div != 0.f) d = __fdiv_rn(d, u.post_div);
+    if (u.mode == 0) {
+      w[i] = __fmaf_rn(-u.lr, d, w[i]);
+    } else {
+      const float gg = __fmaf_rn(u.weight_decay, w[i], d);
+      v[i] = __fmaf_rn(u.momentum, v[i], gg);
+      w[i] = __fmaf_rn(-u.lr, v[i], w[i]);
+    }
+    bad |= !isfinite(w[i]);
+  }
+  *reinterpret_cast<float4*>(u.w + at) = make_float4(w[0], w[1], w[2], w[3]);
+  if (u.mode) *reinterpret_cast<float4*>(u.v + at) = make_float4(v[0], v[1], v[2], v[3]);
+  float h[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = tf32_rna(w[i]);
+  *reinterpret_cast<float4*>(u.hi + at) = make_float4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<float4*>(u.lo + at) =
+      make_float4(tf32_rna(w[0] - h[0]), tf32_rna(w[1] - h[1]), tf32_rna(w[2] - h[2]), tf32_rna(w[3] - h[3]));
+  return bad;
+}
+__device__ __forceinline__ float4 upd_w4(const FusedUpdate& u, int64_t at) {
+  return *reinterpret_cast<const float4*>(u.w + at);
+}
+__device__ __forceinline__ float4 upd_v4(const FusedUpdate& u, int64_t at) {
+  return u.mode ? *reinterpret_cast<const float4*>(u.v + at) : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
 // Epilogue on 4 consecutive columns [col, col + 4) of one row (coalesced: the lanes of a warp cover whole 128 B
 // rows). aux = b[col..col+3] (forward) or the ReLU mask source act[row][col..col+3] (input gradient), loaded by the
 // caller ahead of time (epi_aux) so its latency overlaps the previous chunk.
-__device__ __forceinline__ float4 epi_aux(const EpiParams& ep, int epi, int row, int col) {
-  if (epi == kFwd) return __ldg(reinterpret_cast<const float4*>(ep.bias + col));
-  if (epi == kIgrad) return __ldg(reinterpret_cast<const float4*>(ep.mask + static_cast<int64_t>(row) * ep.ldm + col));
+// EPI is a template parameter throughout: each kernel instantiation carries one epilogue only (a single kernel
+// with every epilogue inlined stalled on instruction fetch).
+template <int EPI>
+__device__ __forceinline__ float4 epi_aux(const EpiParams& ep, int row, int col) {
+  if (EPI == kFwd) return __ldg(reinterpret_cast<const float4*>(ep.bias + col));
+  if (EPI == kIgrad) return __ldg(reinterpret_cast<const float4*>(ep.mask + static_cast<int64_t>(row) * ep.ldm + col));
   return make_float4(0.f, 0.f, 0.f, 0.f);
 }
-__device__ __forceinline__ void epi_vec4(const EpiParams& ep, int epi, int row, int col, float4 v, float4 aux) {
+template <int EPI>
+__device__ __forceinline__ void epi_vec4(const EpiParams& ep, int row, int col, float4 v, float4 aux,
+                                         const BucketScatter& scat_table) {
+  constexpr int epi = EPI;
   const float4 bias4 = aux;
-  if (epi == kRaw) {
-    *reinterpret_cast<float4*>(ep.partial + static_cast<int64_t>(row) * ep.N + col) = v;
-    return;
-  }
   float o[4] = {v.x, v.y, v.z, v.w};
   if (epi == kFwd) {
     const float b[4] = {bias4.x, bias4.y, bias4.z, bias4.w};
@@ -238,7 +288,12 @@ __device__ __forceinline__ void epi_vec4(const EpiParams& ep, int epi, int row, 
       if (!(mk[i] > 0.f)) o[i] = 0.f;
   }
   const int64_t at = static_cast<int64_t>(row) * ep.ldo + col;
-  *reinterpret_cast<float4*>(ep.out + at) = make_float4(o[0], o[1], o[2], o[3]);
+  if (epi == kWgrad && ep.fuse_upd) {
+    if (fused_update4(ep.upd, at, o, upd_w4(ep.upd, at), upd_v4(ep.upd, at))) atomicOr(ep.upd.bad, 1u);
+    return;
+  }
+  float* outp = (epi == kWgrad && ep.scat.n) ? scatter_at(scat_table, ep.scat.e0 + at) : ep.out + at;
+  *reinterpret_cast<float4*>(outp) = make_float4(o[0], o[1], o[2], o[3]);
   if (ep.out_hi) {
     const float h0 = tf32_rna(o[0]), h1 = tf32_rna(o[1]), h2 = tf32_rna(o[2]), h3 = tf32_rna(o[3]);
     *reinterpret_cast<float4*>(ep.out_hi + at) = make_float4(h0, h1, h2, h3);
@@ -252,11 +307,11 @@ __device__ __forceinline__ void epi_vec4(const EpiParams& ep, int epi, int row, 
 // (2 x 256 columns) let the epilogue of tile i overlap the MMAs of tile i+1; the smem stage ring runs continuously
 // across tiles. In pair mode the leader CTA (rank 0) issues the cta_group::2 MMAs and owns the full/tmem-empty
 // barriers; both CTAs load their halves, and the MMA commits multicast to both CTAs' empty/tmem-full barriers.
-template <bool A_MN, bool B_MN, int PAIR>
+template <bool A_MN, bool B_MN, int PAIR, int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
-                       const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo, int epi,
-                       int k_per_split, int splits, EpiParams ep) {
+                       const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
+                       int k_per_split, int splits, const __grid_constant__ EpiParams ep) {
   using C = Cfg<PAIR>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -380,23 +435,34 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int z = t / (mt * nt), r = t % (mt * nt);
       const int m0 = (r % mt) * BM * PAIR + static_cast<int>(rank) * BM, n0 = (r / mt) * BN;
       const uint32_t a = local & 1u;
-      EpiParams e = ep;
-      int mode = epi;
-      if (splits > 1) {
-        mode = kRaw;
-        e.partial = ep.partial + static_cast<int64_t>(z) * ep.M * ep.N;
-      }
+      // scalar fields in registers; the scatter table stays in (grid-constant) param space, where it is indexed
+      const EpiParams e = ep;
+      const bool raw = splits > 1;  // split-K: raw partial planes, the epilogue runs in splitk_reduce
+      float* partial = raw ? ep.partial + static_cast<int64_t>(z) * ep.M * ep.N : nullptr;
       // TMEM gives lane = row; the chunk goes through a swizzled 4 KB smem tile (16 B chunk j of row r at
       // j ^ (r & 7): conflict-free both ways) so each global access of the warp covers 4 whole 128 B rows.
       float4* stg = reinterpret_cast<float4*>(smem + STAGE_RING_BYTES + q * EPI_STAGE_BYTES);
       const int ch = lane & 7;
       float4 aux[8];  // bias / mask operands of the current chunk, prefetched one chunk ahead
 #pragma unroll
-      for (int i = 0; i < 8; ++i) aux[i] = epi_aux(e, mode, m0 + q * 32 + 4 * i + (lane >> 3), n0 + ch * 4);
+      for (int i = 0; i < 8; ++i)
+        aux[i] = raw ? make_float4(0.f, 0.f, 0.f, 0.f) : epi_aux<EPI>(e, m0 + q * 32 + 4 * i + (lane >> 3), n0 + ch * 4);
       mbar_wait(&tfull_bar[a], (local >> 1) & 1u);
       tc_fence_after();
+      // fused update: the chunk's w / v (8 rows x 4 columns per lane) are loaded before the accumulator, into the
+      // registers the bias / mask prefetch uses in the other epilogues
+      const bool fu = EPI == kWgrad && !raw && e.fuse_upd;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
+        float4 nxt[8];
+        if (fu) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int64_t at = static_cast<int64_t>(m0 + q * 32 + 4 * i + (lane >> 3)) * e.ldo + n0 + c + ch * 4;
+            aux[i] = upd_w4(e.upd, at);
+            nxt[i] = upd_v4(e.upd, at);
+          }
+        }
         uint32_t rr[32];
         const uint32_t taddr = tmem + a * TMEM_COLS + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c);
         asm volatile(
@@ -408,10 +474,11 @@ __global__ void __launch_bounds__(THREADS, 1)
               "=r"(rr[22]), "=r"(rr[23]), "=r"(rr[24]), "=r"(rr[25]), "=r"(rr[26]), "=r"(rr[27]), "=r"(rr[28]),
               "=r"(rr[29]), "=r"(rr[30]), "=r"(rr[31])
             : "r"(taddr));
-        float4 nxt[8];
         const int cn = c + 32 < BN ? c + 32 : c;
+        if (!fu && !raw) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) nxt[i] = epi_aux(e, mode, m0 + q * 32 + 4 * i + (lane >> 3), n0 + cn + ch * 4);
+          for (int i = 0; i < 8; ++i) nxt[i] = epi_aux<EPI>(e, m0 + q * 32 + 4 * i + (lane >> 3), n0 + cn + ch * 4);
+        }
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (ep.probe & 1u) continue;
 #pragma unroll
@@ -420,13 +487,34 @@ __global__ void __launch_bounds__(THREADS, 1)
                                                          __uint_as_float(rr[4 * j + 2]), __uint_as_float(rr[4 * j + 3]));
         __syncwarp();
         const int col = n0 + c + ch * 4;
+        if (fu) {
+          bool bad = false;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int rw = 4 * i + (lane >> 3);
-          epi_vec4(e, mode, m0 + q * 32 + rw, col, stg[rw * 8 + (ch ^ (rw & 7))], aux[i]);
+          for (int i = 0; i < 8; ++i) {
+            const int rw = 4 * i + (lane >> 3);
+            const float4 acc = stg[rw * 8 + (ch ^ (rw & 7))];
+            float g[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) g[u] = e.div_pow2 ? g[u] * e.div_inv : __fdiv_rn(g[u], e.div);
+            bad |= fused_update4(e.upd, static_cast<int64_t>(m0 + q * 32 + rw) * e.ldo + col, g, aux[i], nxt[i]);
+          }
+          if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(e.upd.bad, 1u);
+        } else if (raw) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rw = 4 * i + (lane >> 3);
+            *reinterpret_cast<float4*>(partial + static_cast<int64_t>(m0 + q * 32 + rw) * e.N + col) =
+                stg[rw * 8 + (ch ^ (rw & 7))];
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rw = 4 * i + (lane >> 3);
+            epi_vec4<EPI>(e, m0 + q * 32 + rw, col, stg[rw * 8 + (ch ^ (rw & 7))], aux[i], ep.scat);
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) aux[i] = nxt[i];
         }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) aux[i] = nxt[i];
         __syncwarp();
       }
       tc_fence_before();
@@ -450,7 +538,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // Split-K: sum the partial tiles in ascending split order, then the epilogue (deterministic, no atomics).
-__global__ void splitk_reduce_kernel(int splits, int epi, EpiParams ep) {
+template <int EPI>
+__global__ void splitk_reduce_kernel(int splits, const __grid_constant__ EpiParams ep) {
   const int64_t total = static_cast<int64_t>(ep.M) * ep.N / 4;
   for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < total;
        g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -464,7 +553,7 @@ __global__ void splitk_reduce_kernel(int splits, int epi, EpiParams ep) {
       v.z += q.z;
       v.w += q.w;
     }
-    epi_vec4(ep, epi, row, col, v, epi_aux(ep, epi, row, col));
+    epi_vec4<EPI>(ep, row, col, v, epi_aux<EPI>(ep, row, col), ep.scat);
   }
 }
 
@@ -520,7 +609,8 @@ __global__ void softmax_xent_split_kernel(const float* __restrict__ logits, cons
 
 // Bias gradient for the fp32 path: db[j] = (sum_s delta[s, j]) / B. 32 columns x 8 row-partitions per block,
 // partials combined in a fixed order (deterministic, no atomics).
-__global__ void bias_grad_f32_kernel(const float* __restrict__ delta, int b, int n, float* __restrict__ db) {
+__global__ void bias_grad_f32_kernel(const float* __restrict__ delta, int b, int n, float* __restrict__ db,
+                                     const __grid_constant__ BucketScatter scat, const __grid_constant__ FusedUpdate upd) {
   __shared__ float part[8][33];
   const int j = blockIdx.x * 32 + threadIdx.x;
   float acc = 0.f;
@@ -532,7 +622,35 @@ __global__ void bias_grad_f32_kernel(const float* __restrict__ delta, int b, int
     float t = part[0][threadIdx.x];
 #pragma unroll
     for (int q = 1; q < 8; ++q) t += part[q][threadIdx.x];
-    db[j] = __fdiv_rn(t, static_cast<float>(b));
+    t = __fdiv_rn(t, static_cast<float>(b));
+    if (upd.w) {
+      float d = t;
+      if (upd.add_zero) d = __fadd_rn(d, 0.f);
+      if (upd.post_div != 0.f) d = __fdiv_rn(d, upd.post_div);
+      float w = upd.w[j], v = upd.mode ? upd.v[j] : 0.f;
+      if (upd.mode == 0) {
+        w = __fmaf_rn(-upd.lr, d, w);
+      } else {
+        v = __fmaf_rn(upd.momentum, v, __fmaf_rn(upd.weight_decay, w, d));
+        w = __fmaf_rn(-upd.lr, v, w);
+      }
+      upd.w[j] = w;
+      if (upd.mode) upd.v[j] = v;
+      const float h = tf32_rna(w);
+      upd.hi[j] = h;
+      upd.lo[j] = tf32_rna(w - h);
+      if (!isfinite(w)) atomicOr(upd.bad, 1u);
+    } else if (scat.n) {
+      *scatter_at(scat, scat.e0 + j) = t;
+    } else {
+      db[j] = t;
+    }
+  }
+  if (upd.loss_out && blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) {  // the folded loss slot
+    float d = *upd.loss_in;
+    if (upd.add_zero) d = __fadd_rn(d, 0.f);
+    if (upd.post_div != 0.f) d = __fdiv_rn(d, upd.post_div);
+    *upd.loss_out = d;
   }
 }
 
@@ -626,7 +744,7 @@ int sm_count() {
   return sms;
 }
 
-template <bool A_MN, bool B_MN, int PAIR>
+template <bool A_MN, bool B_MN, int PAIR, int EPI>
 void launch_variant(const GemmPlan& p, cudaStream_t st) {
   // the dynamic-smem opt-in is per device: remember which devices this instantiation was configured on
   static std::mutex mu;
@@ -636,7 +754,7 @@ void launch_variant(const GemmPlan& p, cudaStream_t st) {
   {
     std::lock_guard<std::mutex> lk(mu);
     if (!(configured >> dev & 1ull)) {
-      LSGD_CUDA(cudaFuncSetAttribute(gemm_tf32x3_kernel<A_MN, B_MN, PAIR>,
+      LSGD_CUDA(cudaFuncSetAttribute(gemm_tf32x3_kernel<A_MN, B_MN, PAIR, EPI>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
       configured |= 1ull << dev;
     }
@@ -656,16 +774,22 @@ void launch_variant(const GemmPlan& p, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  LSGD_CUDA(cudaLaunchKernelEx(&cfg, gemm_tf32x3_kernel<A_MN, B_MN, PAIR>, p.a_hi, p.a_lo, p.b_hi, p.b_lo, p.epi,
+  LSGD_CUDA(cudaLaunchKernelEx(&cfg, gemm_tf32x3_kernel<A_MN, B_MN, PAIR, EPI>, p.a_hi, p.a_lo, p.b_hi, p.b_lo,
                                p.K / p.splits, p.splits, p.ep));
 }
 
+template <int PAIR, int EPI>
+void launch_pair_epi(const GemmPlan& p, cudaStream_t st) {
+  if (!p.a_mn && !p.b_mn) launch_variant<false, false, PAIR, EPI>(p, st);
+  else if (!p.a_mn && p.b_mn) launch_variant<false, true, PAIR, EPI>(p, st);
+  else if (p.a_mn && p.b_mn) launch_variant<true, true, PAIR, EPI>(p, st);
+  else launch_variant<true, false, PAIR, EPI>(p, st);
+}
 template <int PAIR>
 void launch_pair(const GemmPlan& p, cudaStream_t st) {
-  if (!p.a_mn && !p.b_mn) launch_variant<false, false, PAIR>(p, st);
-  else if (!p.a_mn && p.b_mn) launch_variant<false, true, PAIR>(p, st);
-  else if (p.a_mn && p.b_mn) launch_variant<true, true, PAIR>(p, st);
-  else launch_variant<true, false, PAIR>(p, st);
+  if (p.epi == kFwd) launch_pair_epi<PAIR, kFwd>(p, st);
+  else if (p.epi == kWgrad) launch_pair_epi<PAIR, kWgrad>(p, st);
+  else launch_pair_epi<PAIR, kIgrad>(p, st);
 }
 
 void run_plan(const GemmPlan& p, cudaStream_t st, LaunchCounter& lc) {
@@ -678,7 +802,9 @@ void run_plan(const GemmPlan& p, cudaStream_t st, LaunchCounter& lc) {
   if (p.splits > 1) {
     int64_t work = static_cast<int64_t>(p.M) * p.N / 4;
     int grid = static_cast<int>(std::min<int64_t>((work + 255) / 256, 148 * 8));
-    splitk_reduce_kernel<<<grid, 256, 0, st>>>(p.splits, p.epi, p.ep);
+    if (p.epi == kFwd) splitk_reduce_kernel<kFwd><<<grid, 256, 0, st>>>(p.splits, p.ep);
+    else if (p.epi == kWgrad) splitk_reduce_kernel<kWgrad><<<grid, 256, 0, st>>>(p.splits, p.ep);
+    else splitk_reduce_kernel<kIgrad><<<grid, 256, 0, st>>>(p.splits, p.ep);
     ++lc.n;
     LSGD_CUDA(cudaGetLastError());
   }
@@ -778,11 +904,10 @@ void tc_alloc(TcWorkspace& ws, const Layout& L, int batch, int n_features) {
     ws.act_hi.push_back(dalloc(static_cast<size_t>(B) * L.out(k)));
     ws.act_lo.push_back(dalloc(static_cast<size_t>(B) * L.out(k)));
   }
-  const size_t wide = static_cast<size_t>(B) * std::max(L.widest(), n_features);
-  for (int i = 0; i < 2; ++i) {
-    ws.dlt[i] = dalloc(wide);
-    ws.dlt_hi[i] = dalloc(wide);
-    ws.dlt_lo[i] = dalloc(wide);
+  for (int k = 0; k < L.depth(); ++k) {
+    ws.dlt.push_back(dalloc(static_cast<size_t>(B) * L.out(k)));
+    ws.dlt_hi.push_back(dalloc(static_cast<size_t>(B) * L.out(k)));
+    ws.dlt_lo.push_back(dalloc(static_cast<size_t>(B) * L.out(k)));
   }
   ws.partial_elems = static_cast<size_t>(16) << 20;  // 64 MB of split-K partials
   ws.partial = dalloc(ws.partial_elems);
@@ -796,7 +921,7 @@ void tc_alloc(TcWorkspace& ws, const Layout& L, int batch, int n_features) {
     const float* in_lo = k == 0 ? ws.x_lo : ws.act_lo[static_cast<size_t>(k - 1)];
     const float* wk_hi = ws.w_hi + L.w_off[static_cast<size_t>(k)];
     const float* wk_lo = ws.w_lo + L.w_off[static_cast<size_t>(k)];
-    const int di = (depth - 1 - k) & 1;  // delta of layer k lives in ping-pong slot di
+    const size_t di = static_cast<size_t>(k);  // delta of layer k
     // forward: act_k[B, no] = in[B, ni] . W_k[no, ni]^T + b_k
     {
       EpiParams ep{};
@@ -825,10 +950,10 @@ void tc_alloc(TcWorkspace& ws, const Layout& L, int batch, int n_features) {
     // input grad: delta_{k-1}[B, ni] = (delta_k[B, no] . W_k[no, ni]) * [act_{k-1} > 0]  (W read MN-major)
     if (k > 0) {
       EpiParams ep{};
-      ep.out = ws.dlt[di ^ 1];
+      ep.out = ws.dlt[di - 1];
       ep.ldo = ni;
-      ep.out_hi = ws.dlt_hi[di ^ 1];
-      ep.out_lo = ws.dlt_lo[di ^ 1];
+      ep.out_hi = ws.dlt_hi[di - 1];
+      ep.out_lo = ws.dlt_lo[di - 1];
       ep.mask = ws.act[static_cast<size_t>(k - 1)];
       ep.ldm = ni;
       tl->igrad = make_plan(OpView{ws.dlt_hi[di], B, no, no, false}, ws.dlt_lo[di], OpView{wk_hi, ni, no, ni, true},
@@ -878,7 +1003,7 @@ void tc_head(TcWorkspace& ws, const Layout& L, const int32_t* y, float* sample_l
   const int depth = L.depth();
   const int B = ws.batch;
   const int C = L.out(depth - 1);
-  const int top = 0;  // delta of layer depth-1 lives in ping-pong slot (depth-1-(depth-1)) & 1 = 0
+  const size_t top = static_cast<size_t>(depth - 1);
   softmax_xent_split_kernel<<<(B + 7) / 8, 256, 0, st>>>(ws.act[static_cast<size_t>(depth - 1)], y, B, C,
                                                              ws.dlt[top], ws.dlt_hi[top], ws.dlt_lo[top], sample_loss);
   ++lc.n;
@@ -887,7 +1012,7 @@ void tc_head(TcWorkspace& ws, const Layout& L, const int32_t* y, float* sample_l
 }
 
 void tc_backward_dw(TcWorkspace& ws, const Layout& L, int k, int row0, int rows, float* gW, cudaStream_t st,
-                    LaunchCounter& lc) {
+                    LaunchCounter& lc, const BucketScatter* scat, const FusedUpdate* upd) {
   (void)L;
   TcLayer* tl = ws.layers[static_cast<size_t>(k)];
   auto key = std::make_pair(row0, rows);
@@ -903,12 +1028,20 @@ void tc_backward_dw(TcWorkspace& ws, const Layout& L, int k, int row0, int rows,
   }
   GemmPlan pw = it->second;
   pw.ep.out = gW;
+  if (scat) pw.ep.scat = *scat;
+  if (upd) {
+    pw.ep.fuse_upd = 1;
+    pw.ep.upd = *upd;
+  }
   run_plan(pw, st, lc);
 }
 
-void tc_backward_bias(TcWorkspace& ws, const Layout& L, int k, float* gb, cudaStream_t st, LaunchCounter& lc) {
-  const int di = (L.depth() - 1 - k) & 1;
-  bias_grad_f32_kernel<<<(L.out(k) + 31) / 32, dim3(32, 8), 0, st>>>(ws.dlt[di], ws.batch, L.out(k), gb);
+void tc_backward_bias(TcWorkspace& ws, const Layout& L, int k, float* gb, cudaStream_t st, LaunchCounter& lc,
+                      const BucketScatter* scat, const FusedUpdate* upd) {
+  const size_t di = static_cast<size_t>(k);
+  BucketScatter sc = scat ? *scat : BucketScatter{};
+  FusedUpdate fu = upd ? *upd : FusedUpdate{};
+  bias_grad_f32_kernel<<<(L.out(k) + 31) / 32, dim3(32, 8), 0, st>>>(ws.dlt[di], ws.batch, L.out(k), gb, sc, fu);
   ++lc.n;
   LSGD_CUDA(cudaGetLastError());
 }
@@ -1015,7 +1148,8 @@ void tc_debug_step(const std::vector<int32_t>& layers, int batch, const float* w
                          cudaMemcpyDeviceToHost));
     off += static_cast<int64_t>(batch) * L.out(k);
   }
-  LSGD_CUDA(cudaMemcpy(delta_out, ws.dlt[0], sizeof(float) * batch * L.out(L.depth() - 1), cudaMemcpyDeviceToHost));
+  LSGD_CUDA(cudaMemcpy(delta_out, ws.dlt[static_cast<size_t>(L.depth() - 1)], sizeof(float) * batch * L.out(L.depth() - 1),
+                       cudaMemcpyDeviceToHost));
   for (int k = L.depth() - 1; k >= 0; --k)
     tc_backward_layer(ws, L, k, grad + L.w_off[static_cast<size_t>(k)], grad + L.b_off[static_cast<size_t>(k)], st, lc);
   LSGD_CUDA(cudaDeviceSynchronize());

@@ -27,9 +27,9 @@ struct TcWorkspace {
   float* x_hi = nullptr;       // [B, d]
   float* x_lo = nullptr;
   std::vector<float*> act, act_hi, act_lo;  // [B, out_k] per layer
-  float* dlt[2] = {nullptr, nullptr};       // ping-pong deltas [B, widest]
-  float* dlt_hi[2] = {nullptr, nullptr};
-  float* dlt_lo[2] = {nullptr, nullptr};
+  // deltas [B, out_k] per layer: every dX runs before any dW (the gradient of layer 0 is ready first), so all
+  // layers' deltas are alive at once
+  std::vector<float*> dlt, dlt_hi, dlt_lo;
   float* partial = nullptr;    // split-K workspace
   size_t partial_elems = 0;
   std::vector<TcLayer*> layers;
@@ -51,10 +51,34 @@ void tc_head(TcWorkspace& ws, const Layout& L, const int32_t* y, float* sample_l
 // Backward layer k: dW_k -> gW ([out x in], /B), db_k -> gb, and (k > 0) the masked delta of layer k-1.
 void tc_backward_layer(TcWorkspace& ws, const Layout& L, int k, float* gW, float* gb, cudaStream_t st,
                        LaunchCounter& lc);
+// Gradient-bucket scatter (the first hop of the push exchange fused into the producers): bucket-local element e is
+// written to dst[e / S] + e % S — sub-slice j straight into its owner's stage (over NVLink), the own one locally.
+struct BucketScatter {
+  int n = 0;        // owners (k); 0 = plain local write
+  int64_t S = 0;    // sub-slice length (elements, multiple of 64)
+  int64_t e0 = 0;   // bucket-local index of the first element this producer writes
+  float* dst[kMaxPeers] = {};
+};
+// SGD / momentum update fused into the gradient producers (one worker, one group: the gradient is final as soon as
+// it is produced): the epilogue applies the K8 arithmetic of update_kernel (pre_delta, sgd_one with FMAs, finite
+// check, TF32 split of the new weights) to the bucket's parameters instead of storing the gradient. Pointers are
+// the bucket's first parameter; loss_in -> loss_out copies the (folded) loss slot.
+struct FusedUpdate {
+  float* w = nullptr;
+  float* v = nullptr;
+  float* hi = nullptr;
+  float* lo = nullptr;
+  float lr = 0.f, momentum = 0.f, weight_decay = 0.f, post_div = 0.f;
+  int mode = 0, add_zero = 0;
+  unsigned* bad = nullptr;
+  const float* loss_in = nullptr;
+  float* loss_out = nullptr;
+};
 // The same in pieces: rows [row0, row0+rows) of dW_k -> gW (row stride in_k), then db_k, then dX_k.
 void tc_backward_dw(TcWorkspace& ws, const Layout& L, int k, int row0, int rows, float* gW, cudaStream_t st,
-                    LaunchCounter& lc);
-void tc_backward_bias(TcWorkspace& ws, const Layout& L, int k, float* gb, cudaStream_t st, LaunchCounter& lc);
+                    LaunchCounter& lc, const BucketScatter* scat = nullptr, const FusedUpdate* upd = nullptr);
+void tc_backward_bias(TcWorkspace& ws, const Layout& L, int k, float* gb, cudaStream_t st, LaunchCounter& lc,
+                      const BucketScatter* scat = nullptr, const FusedUpdate* upd = nullptr);
 void tc_backward_dx(TcWorkspace& ws, const Layout& L, int k, cudaStream_t st, LaunchCounter& lc);
 
 // Standalone GEMM for conformance tests: D = A * B^T with A [M x K], B [N x K] given in their storage major

@@ -8,6 +8,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -379,6 +380,97 @@ __global__ void __launch_bounds__(256) push_kernel(const T* __restrict__ src, in
     for (int d = 0; d < n_dst; ++d) dst.p[d][e] = src[e];
 }
 
+// Push-based exchange (all reads local, all cross-GPU traffic as NVLink stores, which need no round trip):
+// dst_d[e] = ((src_0[e] + src_1[e]) + ... [+ 0.0]) [/ divisor] for every destination d (ordered sum, K6/K7), and
+// the pairwise copies of the member -> owner scatter. Grid-capped (they co-run with the GEMMs), so each thread
+// keeps U vectors of every source in flight (NS = source count, 0 = runtime count) to cover HBM latency.
+template <typename T, int NS, int U>
+__global__ void __launch_bounds__(256) reduce_push_kernel(const __grid_constant__ SrcList<T> src, int n_src, int64_t len,
+                                                          const __grid_constant__ DstList<T> dst, int n_dst,
+                                                          bool add_zero, T divisor) {
+  constexpr int V = Vec<T>::kN;
+  constexpr int NSX = NS > 0 ? NS : 1;
+  const int ns = NS > 0 ? NS : n_src;
+  const int64_t nvec = len / V;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < nvec; i0 += U * stride) {
+    Vec<T> acc[U];
+    if (NS > 0) {
+      Vec<T> x[NSX][U];
+#pragma unroll
+      for (int s = 0; s < NSX; ++s)
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (i0 + u * stride < nvec) x[s][u] = ld16(src.p[s] + (i0 + u * stride) * V);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        acc[u] = x[0][u];
+#pragma unroll
+        for (int s = 1; s < NSX; ++s)
+#pragma unroll
+          for (int q = 0; q < V; ++q) acc[u].v[q] = Rn<T>::add(acc[u].v[q], x[s][u].v[q]);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (i0 + u * stride < nvec) acc[u] = ld16(src.p[0] + (i0 + u * stride) * V);
+      for (int s = 1; s < ns; ++s) {
+        Vec<T> x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (i0 + u * stride < nvec) x[u] = ld16(src.p[s] + (i0 + u * stride) * V);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int q = 0; q < V; ++q) acc[u].v[q] = Rn<T>::add(acc[u].v[q], x[u].v[q]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        if (add_zero) acc[u].v[q] = Rn<T>::add(acc[u].v[q], T(0));
+        if (divisor != T(0)) acc[u].v[q] = Rn<T>::div(acc[u].v[q], divisor);
+      }
+    }
+    for (int d = 0; d < n_dst; ++d)
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (i0 + u * stride < nvec) st16(dst.p[d] + (i0 + u * stride) * V, acc[u]);
+  }
+  for (int64_t e = nvec * V + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < len; e += stride) {
+    T a = src.p[0][e];
+    for (int s = 1; s < ns; ++s) a = Rn<T>::add(a, src.p[s][e]);
+    if (add_zero) a = Rn<T>::add(a, T(0));
+    if (divisor != T(0)) a = Rn<T>::div(a, divisor);
+    for (int d = 0; d < n_dst; ++d) dst.p[d][e] = a;
+  }
+}
+
+template <typename T, int U>
+__global__ void __launch_bounds__(256) copy_pairs_kernel(const __grid_constant__ SrcList<T> src,
+                                                         const __grid_constant__ DstList<T> dst, int n_pairs,
+                                                         int64_t len) {
+  constexpr int V = Vec<T>::kN;
+  const int64_t nvec = len / V;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int p = 0; p < n_pairs; ++p) {
+    const T* __restrict__ sp = src.p[p];
+    T* dp = dst.p[p];
+    for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < nvec; i0 += U * stride) {
+      Vec<T> x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (i0 + u * stride < nvec) x[u] = ld16(sp + (i0 + u * stride) * V);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (i0 + u * stride < nvec) st16(dp + (i0 + u * stride) * V, x[u]);
+    }
+    for (int64_t e = nvec * V + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < len; e += stride)
+      dp[e] = sp[e];
+  }
+}
+
 __global__ void signal_many_kernel(SignalList fl, int n, unsigned long long v) {
   __threadfence_system();
   if (threadIdx.x < n) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(fl.f[threadIdx.x]), "l"(v) : "memory");
@@ -482,7 +574,12 @@ void launch_update(const UpdateArgs<T>& a_in, bool exact, cudaStream_t st, Launc
   for (int j = 0; j < kMaxPeers && a.slices.p[j]; ++j) slices_ok = slices_ok && !misaligned(a.slices.p[j]);
   a.scalar_only = (misaligned(a.w) || misaligned(a.v) || misaligned(a.w_hi) || misaligned(a.w_lo) || !slices_ok) ? 1 : 0;
   int64_t work = a.scalar_only ? a.n_params + 1 : a.n_params / Vec<T>::kN + 1;
-  int g = grid_for(work, 256);
+  static const int cap = [] {
+    const char* e = std::getenv("LSGD_B200_UPD_CTAS");
+    const int v = e ? std::atoi(e) : 148 * 8;
+    return v > 0 ? v : 148 * 8;
+  }();
+  int g = grid_for(work, 256, cap);
   if (exact) update_kernel<T, true><<<g, 256, 0, st>>>(a);
   else update_kernel<T, false><<<g, 256, 0, st>>>(a);
   ++lc.n;
@@ -505,6 +602,44 @@ void launch_signal_flag(unsigned long long* flag, unsigned long long value, cuda
 template <typename T>
 void launch_push(const T* src, int64_t len, DstList<T> dst, int n_dst, cudaStream_t st, LaunchCounter& lc) {
   push_kernel<T><<<grid_for(len / Vec<T>::kN + 1, 256, 148 * 2), 256, 0, st>>>(src, len, dst, n_dst);
+  ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
+}
+
+int comm_ctas() {
+  static const int n = [] {
+    const char* e = std::getenv("LSGD_B200_COMM_CTAS");
+    const int v = e ? std::atoi(e) : 148;
+    return v > 0 ? v : 148;
+  }();
+  return n;
+}
+
+template <typename T>
+void launch_reduce_push(SrcList<T> src, int n_src, int64_t len, DstList<T> dst, int n_dst, bool add_zero, T divisor,
+                        cudaStream_t st, LaunchCounter& lc) {
+  bool aligned = true;
+  for (int i = 0; i < n_src; ++i) aligned = aligned && (reinterpret_cast<uintptr_t>(src.p[i]) & 15u) == 0;
+  for (int i = 0; i < n_dst; ++i) aligned = aligned && (reinterpret_cast<uintptr_t>(dst.p[i]) & 15u) == 0;
+  check<Error>(aligned && len % Vec<T>::kN == 0, "reduce_push: slices must be 16-byte aligned vectors");
+  check<Error>(n_src >= 1 && n_src <= kMaxPeers && n_dst >= 1 && n_dst <= kMaxPeers, "reduce_push: bad fan-in/out");
+  constexpr int U = 4;
+  const int g = grid_for(len / Vec<T>::kN / U + 1, 256, comm_ctas());
+  switch (n_src) {
+    case 1: reduce_push_kernel<T, 1, U><<<g, 256, 0, st>>>(src, n_src, len, dst, n_dst, add_zero, divisor); break;
+    case 2: reduce_push_kernel<T, 2, U><<<g, 256, 0, st>>>(src, n_src, len, dst, n_dst, add_zero, divisor); break;
+    case 4: reduce_push_kernel<T, 4, U><<<g, 256, 0, st>>>(src, n_src, len, dst, n_dst, add_zero, divisor); break;
+    default: reduce_push_kernel<T, 0, U><<<g, 256, 0, st>>>(src, n_src, len, dst, n_dst, add_zero, divisor); break;
+  }
+  ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
+}
+
+template <typename T>
+void launch_copy_pairs(SrcList<T> src, DstList<T> dst, int n_pairs, int64_t len, cudaStream_t st, LaunchCounter& lc) {
+  if (n_pairs == 0) return;
+  copy_pairs_kernel<T, 4><<<grid_for(len / Vec<T>::kN / 4 + 1, 256, comm_ctas()), 256, 0, st>>>(src, dst, n_pairs,
+                                                                                                  len);
   ++lc.n;
   LSGD_CUDA(cudaGetLastError());
 }
@@ -547,7 +682,10 @@ void launch_to_f64(const T* src, int64_t n, double* dst, cudaStream_t st, Launch
   template void launch_update<T>(const UpdateArgs<T>&, bool, cudaStream_t, LaunchCounter&);                        \
   template void launch_from_f64<T>(const double*, int64_t, T*, cudaStream_t, LaunchCounter&);                      \
   template void launch_to_f64<T>(const T*, int64_t, double*, cudaStream_t, LaunchCounter&);                       \
-  template void launch_push<T>(const T*, int64_t, DstList<T>, int, cudaStream_t, LaunchCounter&);
+  template void launch_push<T>(const T*, int64_t, DstList<T>, int, cudaStream_t, LaunchCounter&);                 \
+  template void launch_reduce_push<T>(SrcList<T>, int, int64_t, DstList<T>, int, bool, T, cudaStream_t,              \
+                                      LaunchCounter&);                                                             \
+  template void launch_copy_pairs<T>(SrcList<T>, DstList<T>, int, int64_t, cudaStream_t, LaunchCounter&);
 
 LSGD_INSTANTIATE(float)
 LSGD_INSTANTIATE(double)

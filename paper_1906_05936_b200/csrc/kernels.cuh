@@ -11,7 +11,6 @@
 
 namespace lsgd_b200 {
 
-constexpr int kMaxPeers = 16;
 
 // GEMM epilogues of the SIMT path.
 enum GemmEpi : int { kEpiForward = 0, kEpiWeightGrad = 1, kEpiInputGrad = 2 };
@@ -84,6 +83,14 @@ struct DstList {
 };
 template <typename T>
 void launch_push(const T* src, int64_t len, DstList<T> dst, int n_dst, cudaStream_t st, LaunchCounter& lc);
+
+// --- push exchange (K6/K7 without remote reads): ordered sum of local sources written to n destinations (local or
+// peer), and member -> owner scatter copies (pair p: src_p[0, len) -> dst_p). Grids capped at LSGD_B200_COMM_CTAS.
+template <typename T>
+void launch_reduce_push(SrcList<T> src, int n_src, int64_t len, DstList<T> dst, int n_dst, bool add_zero, T divisor,
+                        cudaStream_t st, LaunchCounter& lc);
+template <typename T>
+void launch_copy_pairs(SrcList<T> src, DstList<T> dst, int n_pairs, int64_t len, cudaStream_t st, LaunchCounter& lc);
 
 // --- cross-GPU flags: monotone step counters in peer memory -------------------------------------------------
 struct SignalList {

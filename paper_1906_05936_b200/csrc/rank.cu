@@ -53,9 +53,13 @@ Geometry::Geometry(const RunSpec& spec, int es) : esize(es) {
     const char* env = std::getenv("LSGD_B200_BUCKET_ELEMS");
     const double kBucketElems = env ? std::max(1.0, std::atof(env)) : 16.0 * 1024 * 1024;
     layer_buckets.resize(static_cast<size_t>(L.depth()));
+    // Layer 0's gradient is the last one the backward produces: its exchange + update are the step's exposed tail,
+    // so with an exchange (N > 1) it is cut into blocks of half the size.
+    const double kTailElems = spec.N() > 1 ? kBucketElems / 2 : kBucketElems;
     for (int k = 0; k < L.depth(); ++k) {
       const int in = L.in(k), out = L.out(k);
-      int nc = std::max(1, static_cast<int>(std::ceil(static_cast<double>(in) * out / kBucketElems)));
+      const double target = k == 0 ? kTailElems : kBucketElems;
+      int nc = std::max(1, static_cast<int>(std::ceil(static_cast<double>(in) * out / target)));
       const int quantum = out % 128 == 0 ? 128 : (out % 8 == 0 ? 8 : out);  // GEMM tile rows
       while (nc > 1 && (out % nc != 0 || (out / nc) % quantum != 0)) --nc;
       const int rows = out / nc;
@@ -90,12 +94,17 @@ Geometry::Geometry(const RunSpec& spec, int es) : esize(es) {
   Sg = goff;
   loss_at = buckets.back().poff + buckets.back().n;
   peer.flags = 0;
-  peer.payload = round_up((kArrived + kMaxBuckets * kMaxPeers) * 8, 256);
+  peer.payload = round_up(static_cast<int64_t>(kFlagWords) * 8, 256);
   peer.s[0] = round_up(peer.payload + Ppad * es, 256);
   peer.s[1] = round_up(peer.s[0] + Sg * es, 256);
   peer.gbar = round_up(peer.s[1] + Sg * es, 256);
   peer.gfull = round_up(peer.gbar + Sg * es, 256);
-  peer.total = round_up(peer.gfull + Ppad * es, 256);
+  peer.stage = round_up(peer.gfull + Ppad * es, 256);
+  const int G = spec.G();
+  const int64_t stage_elems = k > 1 ? k * Sg : 0, gstage_elems = G > 1 ? G * Sg : 0;  // only what the layout uses
+  peer.gstage[0] = round_up(peer.stage + stage_elems * es, 256);
+  peer.gstage[1] = round_up(peer.gstage[0] + gstage_elems * es, 256);
+  peer.total = round_up(peer.gstage[1] + gstage_elems * es, 256);
 }
 
 // ================================================================================================ RankImpl
@@ -118,13 +127,16 @@ class RankImpl final : public Rank {
     int major = 0;
     LSGD_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev_));
     check<Error>(major >= 10, "device ", dev_, " is not sm_100-class (compute capability major ", major, ")");
-    LSGD_CUDA(cudaStreamCreateWithFlags(&main_, cudaStreamNonBlocking));
     int lo = 0, hi = 0;
     LSGD_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    // priorities: communicator > compute > updates (the update of most buckets has a step of slack)
+    LSGD_CUDA(cudaStreamCreateWithPriority(&main_, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
     // The communicator role runs on a high-priority side stream; emulated ranks use one stream.
     split_ = workers_.size() == 1;
     if (split_) LSGD_CUDA(cudaStreamCreateWithPriority(&comm_, cudaStreamNonBlocking, hi));
     else comm_ = main_;
+    // a second communicator stream lets consecutive buckets' push exchanges overlap (no NCCL on that path)
+    if (split_) LSGD_CUDA(cudaStreamCreateWithPriority(&comm2_, cudaStreamNonBlocking, hi));
     if (split_) LSGD_CUDA(cudaStreamCreateWithFlags(&upd_, cudaStreamNonBlocking));
     else upd_ = main_;
     for (int b = 0; b < kMaxBuckets; ++b) LSGD_CUDA(cudaEventCreateWithFlags(&ev_upd_[b], cudaEventDisableTiming));
@@ -193,6 +205,7 @@ class RankImpl final : public Rank {
     for (int b = 0; b < kMaxBuckets; ++b) cudaEventDestroy(ev_bucket_[b]);
     if (split_) {
       cudaStreamDestroy(comm_);
+      cudaStreamDestroy(comm2_);
       cudaStreamDestroy(upd_);
     }
     for (int b = 0; b < kMaxBuckets; ++b) cudaEventDestroy(ev_upd_[b]);
@@ -323,6 +336,7 @@ class RankImpl final : public Rank {
   void synchronize() override {
     LSGD_CUDA(cudaSetDevice(dev_));
     LSGD_CUDA(cudaStreamSynchronize(comm_));
+    if (comm2_) LSGD_CUDA(cudaStreamSynchronize(comm2_));
     LSGD_CUDA(cudaStreamSynchronize(upd_));
     LSGD_CUDA(cudaStreamSynchronize(main_));
     check_health();
@@ -375,7 +389,8 @@ class RankImpl final : public Rank {
   int loss_async(void* host_pinned) override {
     LSGD_CUDA(cudaSetDevice(dev_));
     check<Error>(applied_ > 0, "no round has been applied yet");
-    cudaStream_t st = (alg_ == LSGD_B200_LSGD && split_) ? upd_ : main_;  // the stream the round's update ran on
+    // the stream the round's update ran on
+    cudaStream_t st = (alg_ == LSGD_B200_LSGD && split_ && !fused_update()) ? upd_ : main_;
     Timed tm(this, "d2h", st);
     LSGD_CUDA(cudaMemcpyAsync(host_pinned, ws_[0].loss_hist + (applied_ - 1) % kLossCap, sizeof(T),
                               cudaMemcpyDeviceToHost, st));
@@ -391,7 +406,7 @@ class RankImpl final : public Rank {
 
   void join() override {
     LSGD_CUDA(cudaSetDevice(dev_));
-    for (cudaStream_t st : {comm_, upd_, io_}) {
+    for (cudaStream_t st : {comm_, comm2_, upd_, io_}) {
       if (st == nullptr || st == main_) continue;
       LSGD_CUDA(cudaEventRecord(join_ev_, st));
       LSGD_CUDA(cudaStreamWaitEvent(main_, join_ev_, 0));
@@ -495,11 +510,16 @@ class RankImpl final : public Rank {
     int32_t* y = nullptr;
     int32_t* idx = nullptr;
     std::vector<T*> act;
-    T* d0 = nullptr;
-    T* d1 = nullptr;
+    std::vector<T*> dl;  // delta of each layer [B, out_k]
     T* sample_loss = nullptr;
     T* loss_hist = nullptr;
     TcWorkspace tc;  // split-TF32 operands of the tensor-core path
+    const PeerLayout* lay = nullptr;
+    int64_t Sg = 0;
+    T* blk_stage(int m) const { return reinterpret_cast<T*>(blk + lay->stage) + static_cast<int64_t>(m) * Sg; }
+    T* blk_gstage(int par, int g) const {
+      return reinterpret_cast<T*>(blk + lay->gstage[par]) + static_cast<int64_t>(g) * Sg;
+    }
   };
 
   Worker& find(int worker) {
@@ -521,6 +541,8 @@ class RankImpl final : public Rank {
     w.s[1] = reinterpret_cast<T*>(w.blk + geo_.peer.s[1]);
     w.gbar = reinterpret_cast<T*>(w.blk + geo_.peer.gbar);
     w.gfull = reinterpret_cast<T*>(w.blk + geo_.peer.gfull);
+    w.lay = &geo_.peer;
+    w.Sg = geo_.Sg;
     LSGD_CUDA(cudaMalloc(&w.w, sizeof(T) * geo_.P));
     if (spec_.c.mode == LSGD_B200_MOMENTUM) LSGD_CUDA(cudaMalloc(&w.v, sizeof(T) * geo_.P));
     LSGD_CUDA(cudaMalloc(&w.loss_hist, sizeof(T) * kLossCap));
@@ -547,9 +569,11 @@ class RankImpl final : public Rank {
           LSGD_CUDA(cudaMalloc(&a, sizeof(T) * static_cast<size_t>(B_) * L_.out(k)));
           w.act.push_back(a);
         }
-        int wide = std::max(L_.widest(), d);
-        LSGD_CUDA(cudaMalloc(&w.d0, sizeof(T) * static_cast<size_t>(B_) * wide));
-        LSGD_CUDA(cudaMalloc(&w.d1, sizeof(T) * static_cast<size_t>(B_) * wide));
+        for (int k = 0; k < L_.depth(); ++k) {  // per-layer deltas: every dX runs before any dW
+          T* dl = nullptr;
+          LSGD_CUDA(cudaMalloc(&dl, sizeof(T) * static_cast<size_t>(B_) * L_.out(k)));
+          w.dl.push_back(dl);
+        }
       }
     }
     own_x_.push_back(w.x);
@@ -565,8 +589,7 @@ class RankImpl final : public Rank {
     cudaFree(w.loss_hist);
     if (w.idx) cudaFree(w.idx);
     for (T* a : w.act) cudaFree(a);
-    if (w.d0) cudaFree(w.d0);
-    if (w.d1) cudaFree(w.d1);
+    for (T* p : w.dl) cudaFree(p);
     if (w.sample_loss) cudaFree(w.sample_loss);
     tc_free(w.tc);
   }
@@ -732,7 +755,7 @@ class RankImpl final : public Rank {
   // ------------------------------------------------------------------------------------------ compute
   // forward layer k / head / backward layer k of the local shard (mlp.cpp:60-127 as batched GEMMs); the
   // gradient of layer k lands in payload bucket k, the mean loss in the loss slot.
-  T* delta_buf(Worker& w, int k) { return ((L_.depth() - 1 - k) & 1) ? w.d1 : w.d0; }
+  T* delta_buf(Worker& w, int k) { return w.dl[static_cast<size_t>(k)]; }
 
   void forward_layer(Worker& w, int k) {
     if (synth_) return;
@@ -754,9 +777,60 @@ class RankImpl final : public Rank {
                         k + 1 < L_.depth() ? 1 : 0, T(0), nullptr, main_, lc_);
   }
 
+  // The push exchange's scatter is fused into the producers (dW epilogue, bias, loss) on the tensor-core path.
+  bool fused_scatter() const {
+    const bool exchange = !flat_nccl() && !reduce_folded() && alg_ != LSGD_B200_SEQUENTIAL;
+    return exchange && split_ && use_tc_ && k_ > 1;
+  }
+  // One worker, one group (N = 1): the gradient is final when produced, so the update runs in the producers'
+  // epilogues (dW GEMM, bias) and the separate update pass over g disappears.
+  bool fused_update() const {
+    // opt-in (LSGD_B200_FUSED_UPDATE=1): bitwise the separate pass, but its epilogue is latency-bound today
+    static const bool on = std::getenv("LSGD_B200_FUSED_UPDATE") != nullptr;
+    return on && alg_ == LSGD_B200_LSGD && split_ && use_tc_ && reduce_folded() && !spec_.c.record_phases;
+  }
+  FusedUpdate fused_update_args(Worker& w, int64_t first_param, const Bucket* loss_bucket) {
+    FusedUpdate u;
+    u.w = reinterpret_cast<float*>(w.w + first_param);
+    u.v = w.v ? reinterpret_cast<float*>(w.v + first_param) : nullptr;
+    u.hi = w.tc.w_hi + first_param;
+    u.lo = w.tc.w_lo + first_param;
+    u.lr = static_cast<float>(spec_.lr(t_cur_));
+    u.momentum = static_cast<float>(spec_.c.momentum);
+    u.weight_decay = static_cast<float>(spec_.c.weight_decay);
+    u.mode = spec_.c.mode;
+    u.add_zero = 1;  // the communicator's zero (executors.cpp:278), then / N
+    u.post_div = static_cast<float>(N_);
+    u.bad = bad_dev_;
+    if (loss_bucket) {
+      u.loss_in = reinterpret_cast<const float*>(w.payload + geo_.loss_at);
+      u.loss_out = reinterpret_cast<float*>(w.loss_hist + (t_cur_ % kLossCap));
+    }
+    return u;
+  }
+  BucketScatter bucket_scatter(Worker& w, int b, int64_t e0) {
+    const Bucket& bk = geo_.buckets[static_cast<size_t>(b)];
+    const auto members = group_members(w.g);
+    BucketScatter sc;
+    sc.n = k_;
+    sc.S = bk.S;
+    sc.e0 = e0;
+    for (int j = 0; j < k_; ++j)
+      sc.dst[j] = reinterpret_cast<float*>(j == w.j ? w.payload + bk.poff + static_cast<int64_t>(j) * bk.S
+                                                    : peer_stage(members[static_cast<size_t>(j)], w.j) + bk.goff);
+    return sc;
+  }
+
   void head(Worker& w) {
     if (synth_) return;
     T* loss_out = w.payload + geo_.loss_at;
+    if (fused_scatter()) {  // the loss slot (bucket-local index n of the last bucket) goes to its owner
+      const int lb = static_cast<int>(geo_.buckets.size()) - 1;
+      const Bucket& bk = geo_.buckets[static_cast<size_t>(lb)];
+      const BucketScatter sc = bucket_scatter(w, lb, 0);
+      const int j = static_cast<int>(bk.n / bk.S);
+      loss_out = reinterpret_cast<T*>(sc.dst[j] + (bk.n - j * bk.S));
+    }
     Timed tm(this, "head", main_);
     if (use_tc_) {
       tc_head(w.tc, L_, w.y, reinterpret_cast<float*>(w.sample_loss), reinterpret_cast<float*>(loss_out), main_, lc_);
@@ -776,13 +850,30 @@ class RankImpl final : public Rank {
     T* gW = w.payload + bk.poff;
     T* gb = gW + static_cast<int64_t>(bk.rows) * ni;
     if (use_tc_) {
+      const bool fuse = fused_scatter();
+      const bool fupd = fused_update();
       {
         Timed tm(this, "gemm", main_);
-        tc_backward_dw(w.tc, L_, k, bk.row0, bk.rows, reinterpret_cast<float*>(gW), main_, lc_);
+        const BucketScatter sc = fuse ? bucket_scatter(w, b, 0) : BucketScatter{};
+        const FusedUpdate fu = fupd ? fused_update_args(w, bk.pstart, nullptr) : FusedUpdate{};
+        tc_backward_dw(w.tc, L_, k, bk.row0, bk.rows, reinterpret_cast<float*>(gW), main_, lc_, fuse ? &sc : nullptr,
+                       fupd ? &fu : nullptr);
       }
       if (bk.bias) {
         Timed tb(this, "bias", main_);
-        tc_backward_bias(w.tc, L_, k, reinterpret_cast<float*>(gb), main_, lc_);
+        const BucketScatter sc = fuse ? bucket_scatter(w, b, static_cast<int64_t>(bk.rows) * ni) : BucketScatter{};
+        const FusedUpdate fu =
+            fupd ? fused_update_args(w, L_.b_off[static_cast<size_t>(k)], bk.loss ? &bk : nullptr) : FusedUpdate{};
+        tc_backward_bias(w.tc, L_, k, reinterpret_cast<float*>(gb), main_, lc_, fuse ? &sc : nullptr,
+                         fupd ? &fu : nullptr);
+      }
+      if (fuse) {  // this member's sub-slices of bucket b are in their owners' stage
+        const auto members = group_members(w.g);
+        SignalList sl{};
+        int n = 0;
+        for (int j = 0; j < k_; ++j)
+          if (j != w.j) sl.f[n++] = peer_flag_word(members[static_cast<size_t>(j)], kStaged + b * kMaxPeers + w.j);
+        launch_signal_many(sl, n, static_cast<unsigned long long>(t_cur_ + 1), main_, lc_);
       }
       return;
     }
@@ -864,6 +955,109 @@ class RankImpl final : public Rank {
     push_bucket(w, b, t, st);
   }
 
+  // Push exchange of bucket b (one worker per GPU; comm stream). Same arithmetic as reduce_bucket/global_bucket,
+  // but every cross-GPU byte moves as an NVLink store and every sum reads local HBM:
+  //   1. scatter: member i stores its sub-slices j != i into owner j's stage[i] (+ staged flag);
+  //   2. K6: owner i sums stage[0..k-1] (its own sub-slice from its payload) in ascending member order, + 0.0, / N;
+  //   3. G == 1: the sum goes straight into every member's gfull; G > 1 (ordered): into every slot-i owner's
+  //      gstage[par][g] (+ gsum flag), then K7 sums gstage[par][0..G-1] in ascending group order into the members'
+  //      gfull; G > 1 (nccl): NCCL allreduce over the slot owners, then the push;
+  //   4. arrival flags released to every member (the update waits on them).
+  T* peer_stage(int wid, int m) const {
+    return reinterpret_cast<T*>(base(wid) + geo_.peer.stage) + static_cast<int64_t>(m) * geo_.Sg;
+  }
+  T* peer_gstage(int wid, int par, int g) const {
+    return reinterpret_cast<T*>(base(wid) + geo_.peer.gstage[par]) + static_cast<int64_t>(g) * geo_.Sg;
+  }
+  unsigned long long* peer_flag_word(int wid, int idx) const {
+    return reinterpret_cast<unsigned long long*>(base(wid) + geo_.peer.flags) + idx;
+  }
+  void wait_own(Worker& w, int first, int n_words, int skip, unsigned long long target, cudaStream_t st) {
+    FlagList fl{};
+    int n = 0;
+    for (int q = 0; q < n_words; ++q)
+      if (q != skip) fl.f[n++] = w.flags + first + q;
+    if (n) launch_wait_flags(fl, n, target, timeout_ns(), timed_out_dev_, st, lc_);
+  }
+  void exchange_push_bucket(Worker& w, int b, int64_t t, cudaStream_t st) {
+    const Bucket& bk = geo_.buckets[static_cast<size_t>(b)];
+    const int par = static_cast<int>(t & 1);
+    const unsigned long long round = static_cast<unsigned long long>(t + 1);
+    const auto members = group_members(w.g);
+    const int me = w.j;
+    if (k_ > 1 && fused_scatter()) {
+      wait_own(w, kStaged + b * kMaxPeers, k_, me, round, st);  // the producers already scattered (main stream)
+    } else if (k_ > 1) {
+      SrcList<T> src{};
+      DstList<T> dst{};
+      SignalList sl{};
+      int n = 0;
+      for (int j = 0; j < k_; ++j) {
+        if (j == me) continue;
+        src.p[n] = w.payload + bk.poff + static_cast<int64_t>(j) * bk.S;
+        dst.p[n] = peer_stage(members[static_cast<size_t>(j)], me) + bk.goff;
+        sl.f[n] = peer_flag_word(members[static_cast<size_t>(j)], kStaged + b * kMaxPeers + me);
+        ++n;
+      }
+      {
+        Timed tm(this, "scatter", st);
+        launch_copy_pairs<T>(src, dst, n, bk.S, st, lc_);
+      }
+      launch_signal_many(sl, n, round, st, lc_);
+      wait_own(w, kStaged + b * kMaxPeers, k_, me, round, st);
+    }
+    SrcList<T> src{};
+    for (int m = 0; m < k_; ++m)
+      src.p[m] = m == me ? w.payload + bk.poff + static_cast<int64_t>(me) * bk.S : w.blk_stage(m) + bk.goff;
+    DstList<T> gfull{};
+    SignalList arrived{};
+    for (int m = 0; m < k_; ++m) {
+      gfull.p[m] = peer_gfull(members[static_cast<size_t>(m)]) + bk.poff + static_cast<int64_t>(me) * bk.S;
+      arrived.f[m] = peer_arrived(members[static_cast<size_t>(m)], b, me);
+    }
+    const bool lsgd = alg_ == LSGD_B200_LSGD;
+    if (G_ == 1) {
+      Timed tm(this, "reduce", st);
+      launch_reduce_push<T>(src, k_, bk.S, gfull, k_, lsgd, static_cast<T>(N_), st, lc_);
+    } else if (slice_comm_ == nullptr) {
+      DstList<T> gdst{};
+      SignalList gsig{};
+      int n = 0;
+      for (int g = 0; g < G_; ++g) {
+        const int owner = g * k_ + me;
+        gdst.p[g] = peer_gstage(owner, par, w.g) + bk.goff;
+        if (g != w.g) gsig.f[n++] = peer_flag_word(owner, kGsum + b * kMaxPeers + w.g);
+      }
+      {
+        Timed tm(this, "reduce", st);
+        launch_reduce_push<T>(src, k_, bk.S, gdst, G_, lsgd, static_cast<T>(N_), st, lc_);
+      }
+      launch_signal_many(gsig, n, round, st, lc_);
+      wait_own(w, kGsum + b * kMaxPeers, G_, w.g, round, st);
+      SrcList<T> gsrc{};
+      for (int g = 0; g < G_; ++g) gsrc.p[g] = w.blk_gstage(par, g) + bk.goff;
+      Timed tm(this, "global", st);
+      launch_reduce_push<T>(gsrc, G_, bk.S, gfull, k_, false, T(0), st, lc_);
+    } else {
+      DstList<T> sdst{};
+      sdst.p[0] = w.s[par] + bk.goff;
+      {
+        Timed tm(this, "reduce", st);
+        launch_reduce_push<T>(src, k_, bk.S, sdst, 1, lsgd, static_cast<T>(N_), st, lc_);
+      }
+      {
+        Timed tm(this, "global", st);
+        LSGD_NCCL(ncclAllReduce(w.s[par] + bk.goff, w.gbar + bk.goff, static_cast<size_t>(bk.S), nccl_type(),
+                                ncclSum, slice_comm_, st));
+      }
+      SrcList<T> one{};
+      one.p[0] = w.gbar + bk.goff;
+      Timed tm(this, "broadcast", st);
+      launch_reduce_push<T>(one, 1, bk.S, gfull, k_, false, T(0), st, lc_);
+    }
+    launch_signal_many(arrived, k_, round, st, lc_);
+  }
+
   // K8 for bucket b of round u (executors.cpp:210-229): pull the k averaged sub-slices of the group, apply
   // sgd_update to the bucket's parameters, check finiteness, record the loss (last bucket).
   void apply_bucket(Worker& w, int b, int64_t u, cudaStream_t st) {
@@ -915,6 +1109,7 @@ class RankImpl final : public Rank {
 
   // ------------------------------------------------------------------------------------------ one step
   void issue_one(int64_t t, const int32_t* given, bool shard_only) {
+    t_cur_ = t;
     const int D = synth_ ? 1 : L_.depth();
     const int NB = nb_;
     const auto& LB = geo_.layer_buckets;
@@ -934,7 +1129,7 @@ class RankImpl final : public Rank {
       phase_mark(widx(w), t, 1, 0, main_);
       for (int k = 0; k < D; ++k) {
         for (int b : LB[static_cast<size_t>(k)]) {
-          if (eager && t >= 1) {
+          if (eager && t >= 1 && !fused_update()) {
             LSGD_CUDA(cudaStreamWaitEvent(main_, ev_upd_[b], 0));
           } else if (postponed) {
             current_phase() = "broadcast";
@@ -946,40 +1141,33 @@ class RankImpl final : public Rank {
       }
       if (postponed) after_update(w, t - 1, main_);
       head(w);
-      for (int k = D - 1; k >= 0; --k) {
-        // dX_k first: after it W_k is no longer read by this step, so each row block's update (eager) can follow
-        // its dW block immediately, overlapping the remaining weight-gradient GEMMs
+      // Backward: all input gradients first (dX_{D-1} .. dX_1: the delta chain), then the weight gradients from layer
+      // 0 upwards. Layer 0's gradient — the first parameters the next forward needs — is then ready first, so its
+      // exchange and update run under the remaining dW GEMMs, and the last ones (the small top layer) hide under the
+      // next step's first forward GEMMs. Same kernels, same arithmetic; only the order differs.
+      for (int k = D - 1; k >= 1; --k) {
         if (!synth_) backward_input(w, k);
-        if (eager) {
-          LSGD_CUDA(cudaEventRecord(ev_dx_[k], main_));
-          LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_dx_[k], 0));
-        }
+      }
+      if (eager)
+        for (int k = 0; k < D; ++k) LSGD_CUDA(cudaEventRecord(ev_dx_[k], main_));  // no W_k is read any more
+      for (int k = 0; k < D; ++k) {
         for (int b : LB[static_cast<size_t>(k)]) {
           if (!synth_) backward_bucket(w, b);  // row block of dW_k (+ db_k): ready for the exchange right away
-          if (exchange) signal(w, kFlagGrad, b, static_cast<unsigned long long>(t + 1), main_);
+          if (exchange && !split_) signal(w, kFlagGrad, b, static_cast<unsigned long long>(t + 1), main_);
           if (split_) LSGD_CUDA(cudaEventRecord(ev_bucket_[b], main_));
-          if (eager) {
-            current_phase() = "broadcast";
-            if (reduce_folded()) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_bucket_[b], 0));
-            apply_bucket(w, b, t, upd_);
-            LSGD_CUDA(cudaEventRecord(ev_upd_[b], upd_));
-            current_phase() = "compute";
-          }
         }
       }
-      if (eager) after_update(w, t, upd_);
       phase_mark(widx(w), t, 1, 1, main_);
     }
-    if (eager) ++applied_;
     if (rows_slot_ >= 0) {  // this step's staged host rows are no longer read
       LSGD_CUDA(cudaEventRecord(ev_rows_free_[rows_slot_], main_));
       rows_slot_ = -1;
     }
     if (postponed) ++applied_;
 
-    // exchange order: the order buckets finish in the backward (layers descending, row blocks ascending)
+    // exchange order: the order buckets finish in the backward (layers ascending, row blocks ascending)
     std::vector<int> order;
-    for (int k = D - 1; k >= 0; --k)
+    for (int k = 0; k < D; ++k)
       for (int b : LB[static_cast<size_t>(k)]) order.push_back(b);
 
     // communicator work: per bucket, on the comm stream (overlapping the rest of the backward)
@@ -993,14 +1181,21 @@ class RankImpl final : public Rank {
       for (auto& w : ws_) phase_mark(widx(w), t, 2, 0, comm_);
       if (split_) {
         Worker& w = ws_[0];
+        // with the ordered push sum (no NCCL) consecutive buckets alternate between two streams so one bucket's
+        // reduce/global phases overlap the next one's scatter; NCCL collectives keep a single stream (one order)
+        const int n_streams = (slice_comm_ == nullptr && comm2_ != nullptr) ? 2 : 1;
         for (size_t q = 0; q < order.size(); ++q) {
           const int b = order[q];
-          LSGD_CUDA(cudaStreamWaitEvent(comm_, ev_bucket_[b], 0));
-          if (q == 0) launch_sleep(spec_.c.global_link_delay_s, comm_, lc_);
-          reduce_bucket(w, b, t, comm_);
-          current_phase() = "global_allreduce";
-          global_bucket(w, b, t, comm_);
-          current_phase() = "local_reduce";
+          cudaStream_t cs = (n_streams == 2 && (q & 1)) ? comm2_ : comm_;
+          LSGD_CUDA(cudaStreamWaitEvent(cs, ev_bucket_[b], 0));
+          if (q == 0) {
+            launch_sleep(spec_.c.global_link_delay_s, comm_, lc_);
+            if (n_streams == 2) {  // the injected link delay precedes every bucket's exchange
+              LSGD_CUDA(cudaEventRecord(join_ev_, comm_));
+              LSGD_CUDA(cudaStreamWaitEvent(comm2_, join_ev_, 0));
+            }
+          }
+          exchange_push_bucket(w, b, t, cs);
         }
       } else {
         // emulated ranks share one stream: every local slice sum is published before any global average waits
@@ -1012,6 +1207,28 @@ class RankImpl final : public Rank {
           for (auto& w : ws_) global_bucket(w, b, t, main_);
       }
       for (auto& w : ws_) phase_mark(widx(w), t, 3, 1, comm_);
+    }
+
+    // Eager update of round t on the update stream, in backward order. Host issue order matters: these may spin on
+    // the exchange's arrival flags, so they are enqueued after all the work they depend on (this step's backward
+    // and communicator work) — a spinning kernel queued ahead of its producer could block it if the two streams
+    // share a hardware queue.
+    if (eager && fused_update()) {  // already applied by the gradient producers on the main stream
+      after_update(ws_[0], t, main_);
+      ++applied_;
+    } else if (eager) {
+      Worker& w = ws_[0];
+      current_phase() = "broadcast";
+      for (int k = 0; k < D; ++k) {
+        LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_dx_[k], 0));  // W_k is no longer read by this step
+        for (int b : LB[static_cast<size_t>(k)]) {
+          if (reduce_folded()) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_bucket_[b], 0));
+          apply_bucket(w, b, t, upd_);
+          LSGD_CUDA(cudaEventRecord(ev_upd_[b], upd_));
+        }
+      }
+      after_update(w, t, upd_);
+      ++applied_;
     }
 
     if (alg_ != LSGD_B200_LSGD) {  // sequential / csgd: synchronous update in the same block (executors.cpp:172-177)
@@ -1047,7 +1264,7 @@ class RankImpl final : public Rank {
   int64_t hist_rows_;
   int N_ = 1, G_ = 1, k_ = 1, nb_ = 1, alg_ = 2, B_ = 1;
   bool exact_ = false, synth_ = false, split_ = false, use_tc_ = false;
-  cudaStream_t main_ = nullptr, comm_ = nullptr;
+  cudaStream_t main_ = nullptr, comm_ = nullptr, comm2_ = nullptr;
   cudaEvent_t ev_bucket_[kMaxBuckets] = {};
   cudaEvent_t ev_upd_[kMaxBuckets] = {};
   cudaEvent_t ev_dx_[kMaxBuckets] = {};
@@ -1081,6 +1298,7 @@ class RankImpl final : public Rank {
   int* timed_out_dev_ = nullptr;
   unsigned* bad_dev_ = nullptr;
   int64_t t_next_ = 0, applied_ = 0;
+  int64_t t_cur_ = 0;  // step being issued (round counter of the producers' staged flags)
   T* hist_ = nullptr;
   LaunchCounter lc_;
   bool timing_ = false;

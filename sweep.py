@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--sizes", default="20,22,24,26,28,30", help="log2 of P")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--global-allreduce", default="ordered", choices=["ordered", "nccl"])
     args = ap.parse_args()
 
     import torch
@@ -64,6 +65,7 @@ def main():
                                iterations=1 << 30, mode="momentum", layer_sizes=[32, 16, 10])
         cfg.b200.model = "synthetic_gradient"
         cfg.b200.synthetic_params = P
+        cfg.b200.global_allreduce = args.global_allreduce
         r = Rank(cfg, rank, local)
         r.connect(gather(r.export()))
         r.step(args.warmup)
@@ -73,7 +75,7 @@ def main():
         r.timing(True)
         r.step(args.steps)
         r.synchronize()
-        fam = {f: r.kernel_time(f) for f in ("reduce", "global", "broadcast", "update")}
+        fam = {f: r.kernel_time(f) for f in ("scatter", "reduce", "global", "broadcast", "update")}
         r.timing(False)
         per_step = {f: (ms * cnt / args.steps) for f, (ms, cnt) in fam.items()}
         all_ps = gather(per_step)
@@ -87,9 +89,11 @@ def main():
             def gbs(nbytes, ms):
                 return nbytes / (ms * 1e-3) / 1e9 if ms > 0 else None
 
-            line["reduce_nvlink_gbs"] = gbs((k - 1) * S, worst["reduce"]) if k > 1 else None
+            line["scatter_nvlink_gbs"] = gbs((k - 1) * S, worst["scatter"]) if k > 1 else None
+            line["reduce_push_gbs"] = gbs((G - 1) * S, worst["reduce"]) if G > 1 else None
             line["push_nvlink_gbs"] = gbs((k - 1) * S, worst["broadcast"]) if k > 1 else None
             line["global_busbw_gbs"] = gbs(2 * (G - 1) / G * S, worst["global"]) if G > 1 else None
+            line["global_allreduce"] = args.global_allreduce
             line["update_hbm_gbs"] = gbs(20.0 * P, worst["update"])
             line["nvlink_peak_gbs"] = NVLINK_GBS
             line["hbm_peak_gbs"] = hbm

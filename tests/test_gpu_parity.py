@@ -231,6 +231,39 @@ def test_multi_gpu_matches_reference(name, glob, n_gpus):
     assert np.array_equal(r1.final_params.view(np.uint64), r.final_params.view(np.uint64))
 
 
+@pytest.mark.multigpu
+@pytest.mark.parametrize("groups,per_group,dtype,glob", [(4, 1, "fp64", "ordered"), (1, 4, "fp64", "ordered"),
+                                                         (2, 2, "fp32", "ordered"), (2, 2, "fp32", "nccl")])
+def test_multi_gpu_push_exchange_vs_oracle(groups, per_group, dtype, glob, n_gpus, monkeypatch):
+    """One worker per GPU runs the push exchange (scatter -> owner ordered sum -> group-sum push -> ordered global
+    sum -> gfull push). fp64: per-coordinate vs the oracle (G = 4 / k = 4 make the summation order observable);
+    fp32 on a tensor-core-eligible MLP with row-block buckets: norm-wise."""
+    n = groups * per_group
+    if n_gpus < n:
+        pytest.skip(f"needs {n} GPUs")
+    if dtype == "fp32":
+        monkeypatch.setenv("LSGD_B200_BUCKET_ELEMS", "20000")
+        cfg = lsgd.TrainConfig(algorithm="lsgd", n_workers=n, n_groups=groups, layer_sizes=[256, 512, 256],
+                               n_samples=4096, n_features=256, n_classes=256, spread=6.0, mode="momentum",
+                               local_batch=128, iterations=10, record_history=True)
+    else:
+        cfg = lsgd.TrainConfig(algorithm="lsgd", n_workers=n, n_groups=groups, layer_sizes=[16, 24, 8], n_samples=512,
+                               n_features=16, n_classes=8, spread=6.0, mode="momentum", local_batch=8, iterations=12,
+                               record_history=True)
+    cfg.b200.dtype = dtype
+    cfg.b200.n_devices = n
+    cfg.b200.global_allreduce = glob
+    r = lsgd.run_train(cfg)
+    from oracle import Oracle, TrainSpec
+    spec = TrainSpec(**{k: getattr(cfg, k) for k in TrainSpec.__dataclass_fields__ if hasattr(cfg, k)})
+    ref = Oracle("port").run_train(spec, history=True)["history"]
+    e = compare_histories(ref, r.param_history, "push")
+    assert (e.max_rel_deviation if dtype == "fp64" else e.max_normwise_deviation) <= \
+        (FP64_TOL if dtype == "fp64" else FP32_TOL), e
+    for w in range(1, n):
+        assert np.array_equal(r.worker_finals[0].view(np.uint32), r.worker_finals[w].view(np.uint32))
+
+
 @pytest.mark.parametrize("dtype,tol", [("fp64", FP64_TOL), ("fp32", FP32_TOL)])
 def test_row_block_buckets_keep_parity(dtype, tol, monkeypatch):
     """Large layers are exchanged in row blocks (sub-buckets); force several blocks on a small model and check the

@@ -1,6 +1,10 @@
 """Tensor-core (tcgen05 split-TF32) path: GEMM conformance against float64 products, and the fp32 training step
 on a tc-eligible MLP against the fp64 oracle (norm-wise 1e-5, the same contract as the SIMT path)."""
 import ctypes as C
+import os
+import subprocess
+import sys
+import tempfile
 
 import numpy as np
 import pytest
@@ -9,6 +13,7 @@ import paper_1906_05936_b200 as lsgd
 from paper_1906_05936_b200 import _native as N
 
 pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 _fn = N.lib.lsgd_b200_test_gemm
 _fn.argtypes = [C.c_int32] * 6 + [C.c_void_p] * 4 + [C.c_float, C.c_int32, C.c_void_p]
@@ -110,3 +115,32 @@ def test_tc_training_matches_oracle_normwise(mode):
     assert np.linalg.norm(rs.final_params - r.final_params) / np.linalg.norm(rs.final_params) <= 2e-5
     for w in range(1, cfg.n_workers):
         assert np.array_equal(r.worker_finals[0].view(np.uint64), r.worker_finals[w].view(np.uint64))
+
+
+@pytest.mark.parametrize("mode", ["plain", "momentum"])
+def test_single_worker_fused_update_is_bitwise_the_update_pass(mode):
+    """One worker (N = 1): with LSGD_B200_FUSED_UPDATE the update runs inside the dW / bias epilogues. It must give
+    bitwise the iterates of the separate update kernel (the default) and stay within 1e-5 of the oracle."""
+    from oracle import Oracle, TrainSpec
+
+    cfg = tc_cfg(mode=mode, n_workers=1, iterations=12)
+    cfg.b200.gemm = "tcgen05"
+    sep = lsgd.run_train(cfg)
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_1906_05936_b200 as lsgd\n"
+        "c = lsgd.TrainConfig(algorithm='lsgd', n_workers=1, n_groups=1, layer_sizes=[256, 512, 256],\n"
+        "    n_samples=2048, n_features=256, n_classes=256, spread=10.0, local_batch=128, iterations=12,\n"
+        "    mode=%r, record_history=True)\n"
+        "c.b200.n_devices = 1; c.b200.global_allreduce = 'ordered'; c.b200.gemm = 'tcgen05'\n"
+        "np.save(sys.argv[1], lsgd.run_train(c).param_history)\n" % (ROOT, mode))
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "h.npy")
+        env = dict(os.environ, LSGD_B200_FUSED_UPDATE="1")
+        subprocess.run([sys.executable, "-c", code, out], check=True, env=env, cwd=ROOT)
+        fused = np.load(out)
+    assert np.array_equal(fused.view(np.uint64), sep.param_history.view(np.uint64))
+    spec = TrainSpec(**{k: getattr(cfg, k) for k in TrainSpec.__dataclass_fields__ if hasattr(cfg, k)})
+    ref = Oracle("port").run_train(spec, history=True)["history"]
+    dev = np.linalg.norm(fused - ref, axis=1) / np.linalg.norm(ref, axis=1)
+    assert dev.max() <= 1e-5, dev.max()

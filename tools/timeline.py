@@ -16,6 +16,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="cfg3")
     ap.add_argument("--algo", default="lsgd")
+    ap.add_argument("--global-allreduce", default="ordered")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--rows", action="store_true", help="e2e path: pinned host rows (step_rows) + async loss D2H")
@@ -41,7 +42,7 @@ def main():
         pg.all_gather_object(out, o)
         return out
 
-    cfg = bench.workload(args.workload, world, None, args.algo)
+    cfg = bench.workload(args.workload, world, None, args.algo, args.global_allreduce)
     r = Rank(cfg, rank, local)
     r.connect(allgather(r.export()))
     if args.rows:
