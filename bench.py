@@ -20,6 +20,7 @@ reduce, inter-group NCCL average on the side stream.
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
 import subprocess
@@ -301,8 +302,17 @@ def run_b200_arm(args):
             gemm_ms = avg * cnt / args.steps  # per-layer brackets summed to one step's GEMM time
             ach = (B * F) / (gemm_ms / 1e3) / 1e12 if gemm_ms else None
             peak = peaks.get("bf16_tflops_sustained") or 1400.0
+            traffic, tsrc = None, None
+            for cand in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_gemm.json")), reverse=True):
+                try:  # DRAM bytes of one step's GEMM sequence from the committed ncu --set full capture
+                    traffic = json.load(open(cand))["step_gemm_dram_mb"] * 1e6
+                    tsrc = os.path.relpath(cand, ROOT)
+                    break
+                except (OSError, ValueError, KeyError):
+                    pass
             roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                    "frac": (ach / peak) if ach else None, "traffic": None,
+                    "frac": (ach / peak) if ach else None, "traffic": traffic, "traffic_source": tsrc,
+                    "traffic_unit": "bytes DRAM read+write per launch (= one step's GEMM sequence)",
                     "kernel": "forward+backward GEMM sequence per step (B_loc*F flops / its device time)",
                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (3xTF32 ceiling = peak/6)",
                     "flops_per_launch": B * F, "launches_timed": gemm_n}

@@ -45,7 +45,7 @@ constexpr int SMEM_BYTES = STAGE_RING_BYTES + 4 * EPI_STAGE_BYTES + 1024;  // + 
 constexpr uint32_t TMEM_COLS = 256;
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // clears the CTA-rank bit of a shared::cluster address -> leader CTA
 
-enum : int { kFwd = 0, kWgrad = 1, kIgrad = 2, kRaw = 3 };
+enum : int { kFwd = 0, kWgrad = 1, kIgrad = 2, kRaw = 3, kWgradUpd = 4 };  // kWgradUpd: dW + fused update
 
 struct EpiParams {
   float* out;
@@ -278,7 +278,7 @@ __device__ __forceinline__ void epi_vec4(const EpiParams& ep, int row, int col, 
       o[i] = __fadd_rn(o[i], b[i]);
       if (ep.relu && o[i] < 0.f) o[i] = 0.f;
     }
-  } else if (epi == kWgrad) {
+  } else if (epi == kWgrad || epi == kWgradUpd) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) o[i] = ep.div_pow2 ? o[i] * ep.div_inv : __fdiv_rn(o[i], ep.div);  // x*2^-k == x/2^k
   } else {
@@ -288,7 +288,7 @@ __device__ __forceinline__ void epi_vec4(const EpiParams& ep, int row, int col, 
       if (!(mk[i] > 0.f)) o[i] = 0.f;
   }
   const int64_t at = static_cast<int64_t>(row) * ep.ldo + col;
-  if (epi == kWgrad && ep.fuse_upd) {
+  if (epi == kWgradUpd) {
     if (fused_update4(ep.upd, at, o, upd_w4(ep.upd, at), upd_v4(ep.upd, at))) atomicOr(ep.upd.bad, 1u);
     return;
   }
@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_after();
       // fused update: the chunk's w / v (8 rows x 4 columns per lane) are loaded before the accumulator, into the
       // registers the bias / mask prefetch uses in the other epilogues
-      const bool fu = EPI == kWgrad && !raw && e.fuse_upd;
+      const bool fu = EPI == kWgradUpd && !raw;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         float4 nxt[8];
@@ -788,6 +788,7 @@ void launch_pair_epi(const GemmPlan& p, cudaStream_t st) {
 template <int PAIR>
 void launch_pair(const GemmPlan& p, cudaStream_t st) {
   if (p.epi == kFwd) launch_pair_epi<PAIR, kFwd>(p, st);
+  else if (p.epi == kWgrad && p.ep.fuse_upd) launch_pair_epi<PAIR, kWgradUpd>(p, st);
   else if (p.epi == kWgrad) launch_pair_epi<PAIR, kWgrad>(p, st);
   else launch_pair_epi<PAIR, kIgrad>(p, st);
 }
@@ -803,6 +804,7 @@ void run_plan(const GemmPlan& p, cudaStream_t st, LaunchCounter& lc) {
     int64_t work = static_cast<int64_t>(p.M) * p.N / 4;
     int grid = static_cast<int>(std::min<int64_t>((work + 255) / 256, 148 * 8));
     if (p.epi == kFwd) splitk_reduce_kernel<kFwd><<<grid, 256, 0, st>>>(p.splits, p.ep);
+    else if (p.epi == kWgrad && p.ep.fuse_upd) splitk_reduce_kernel<kWgradUpd><<<grid, 256, 0, st>>>(p.splits, p.ep);
     else if (p.epi == kWgrad) splitk_reduce_kernel<kWgrad><<<grid, 256, 0, st>>>(p.splits, p.ep);
     else splitk_reduce_kernel<kIgrad><<<grid, 256, 0, st>>>(p.splits, p.ep);
     ++lc.n;
