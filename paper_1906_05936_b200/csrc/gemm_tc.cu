@@ -33,19 +33,24 @@ constexpr int BM = 128, BN = 256, BK = 16, THREADS = 192;
 constexpr int MN_CHUNK_BYTES = BK * 128;  // one 32-wide MN chunk of an MN-major tile: BK rows of 128 B
 constexpr int A_BYTES = BM * BK * 4;      // 8 KB
 constexpr int STAGE_RING_BYTES = 192 * 1024;
-template <int PAIR>
+constexpr int EPI_STAGE_BYTES = 32 * 32 * 4;  // per epilogue warp: one 32 x 32 fp32 chunk (4 KB)
+// fused update: per epilogue warp, w and v of one 32 x 32 chunk (8 KB), double-buffered (cp.async one chunk ahead)
+constexpr int UPD_PREF_BYTES = 2 * 2 * EPI_STAGE_BYTES;
+enum : int { kFwd = 0, kWgrad = 1, kIgrad = 2, kRaw = 3, kWgradUpd = 4 };  // kWgradUpd: dW + fused update
+template <int PAIR, int EPI = kFwd>
 struct Cfg {
   static constexpr int B_ROWS = BN / PAIR;                          // B rows staged by one CTA
   static constexpr int B_BYTES = B_ROWS * BK * 4;                   // 16 KB | 8 KB
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;     // 48 KB | 32 KB (hi + lo of both operands)
-  static constexpr int STAGES = STAGE_RING_BYTES / STAGE_BYTES;     // 4 | 6
+  // the fused-update epilogue trades mainloop stages (K = B is short) for its w/v staging
+  static constexpr int STAGES = EPI == kWgradUpd ? (PAIR == 2 ? 4 : 3) : STAGE_RING_BYTES / STAGE_BYTES;  // 4 | 6
+  static constexpr int RING = STAGES * STAGE_BYTES;
+  static constexpr int PREF = EPI == kWgradUpd ? 4 * UPD_PREF_BYTES : 0;
+  static constexpr int SMEM = RING + 4 * EPI_STAGE_BYTES + PREF + 1024;  // + alignment slack
+  static_assert(SMEM <= 232448, "dynamic shared memory over the sm_100 limit");
 };
-constexpr int EPI_STAGE_BYTES = 32 * 32 * 4;  // per epilogue warp: one 32 x 32 fp32 chunk (4 KB)
-constexpr int SMEM_BYTES = STAGE_RING_BYTES + 4 * EPI_STAGE_BYTES + 1024;  // + alignment slack
 constexpr uint32_t TMEM_COLS = 256;
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // clears the CTA-rank bit of a shared::cluster address -> leader CTA
-
-enum : int { kFwd = 0, kWgrad = 1, kIgrad = 2, kRaw = 3, kWgradUpd = 4 };  // kWgradUpd: dW + fused update
 
 struct EpiParams {
   float* out;
@@ -136,6 +141,9 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
+}
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(smem_dst)), "l"(gmem_src) : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -312,7 +320,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                        const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
                        int k_per_split, int splits, const __grid_constant__ EpiParams ep) {
-  using C = Cfg<PAIR>;
+  using C = Cfg<PAIR, EPI>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -441,28 +449,34 @@ __global__ void __launch_bounds__(THREADS, 1)
       float* partial = raw ? ep.partial + static_cast<int64_t>(z) * ep.M * ep.N : nullptr;
       // TMEM gives lane = row; the chunk goes through a swizzled 4 KB smem tile (16 B chunk j of row r at
       // j ^ (r & 7): conflict-free both ways) so each global access of the warp covers 4 whole 128 B rows.
-      float4* stg = reinterpret_cast<float4*>(smem + STAGE_RING_BYTES + q * EPI_STAGE_BYTES);
+      float4* stg = reinterpret_cast<float4*>(smem + C::RING + q * EPI_STAGE_BYTES);
       const int ch = lane & 7;
       float4 aux[8];  // bias / mask operands of the current chunk, prefetched one chunk ahead
 #pragma unroll
       for (int i = 0; i < 8; ++i)
         aux[i] = raw ? make_float4(0.f, 0.f, 0.f, 0.f) : epi_aux<EPI>(e, m0 + q * 32 + 4 * i + (lane >> 3), n0 + ch * 4);
+      // fused update: w / v of the lane's 8 rows x 4 columns stream into a per-warp smem double buffer with
+      // cp.async one chunk ahead (chunk 0 before the accumulator is even ready), so the epilogue keeps a chunk of
+      // loads in flight instead of one round trip per chunk
+      const bool fu = EPI == kWgradUpd && !raw;
+      float4* pref = reinterpret_cast<float4*>(smem + C::RING + 4 * EPI_STAGE_BYTES + q * UPD_PREF_BYTES);
+      auto prefetch_wv = [&](int cc) {
+        float4* buf = pref + ((cc / 32) & 1) * 512;  // [w: 8 x 32 | v: 8 x 32] float4 per buffer
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int64_t at = static_cast<int64_t>(m0 + q * 32 + 4 * i + (lane >> 3)) * e.ldo + n0 + cc + ch * 4;
+          cp_async16(buf + i * 32 + lane, e.upd.w + at);
+          if (e.upd.mode) cp_async16(buf + 256 + i * 32 + lane, e.upd.v + at);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      };
+      if (fu) prefetch_wv(0);
       mbar_wait(&tfull_bar[a], (local >> 1) & 1u);
       tc_fence_after();
-      // fused update: the chunk's w / v (8 rows x 4 columns per lane) are loaded before the accumulator, into the
-      // registers the bias / mask prefetch uses in the other epilogues
-      const bool fu = EPI == kWgradUpd && !raw;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         float4 nxt[8];
-        if (fu) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int64_t at = static_cast<int64_t>(m0 + q * 32 + 4 * i + (lane >> 3)) * e.ldo + n0 + c + ch * 4;
-            aux[i] = upd_w4(e.upd, at);
-            nxt[i] = upd_v4(e.upd, at);
-          }
-        }
+        if (fu && c + 32 < BN) prefetch_wv(c + 32);
         uint32_t rr[32];
         const uint32_t taddr = tmem + a * TMEM_COLS + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c);
         asm volatile(
@@ -488,6 +502,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         __syncwarp();
         const int col = n0 + c + ch * 4;
         if (fu) {
+          // this chunk's w / v group has landed (the next chunk's may still be in flight)
+          if (c + 32 < BN) asm volatile("cp.async.wait_group 1;" ::: "memory");
+          else asm volatile("cp.async.wait_group 0;" ::: "memory");
+          const float4* buf = pref + ((c / 32) & 1) * 512;
           bool bad = false;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -496,7 +514,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             float g[4] = {acc.x, acc.y, acc.z, acc.w};
 #pragma unroll
             for (int u = 0; u < 4; ++u) g[u] = e.div_pow2 ? g[u] * e.div_inv : __fdiv_rn(g[u], e.div);
-            bad |= fused_update4(e.upd, static_cast<int64_t>(m0 + q * 32 + rw) * e.ldo + col, g, aux[i], nxt[i]);
+            const float4 v4 = e.upd.mode ? buf[256 + i * 32 + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+            bad |= fused_update4(e.upd, static_cast<int64_t>(m0 + q * 32 + rw) * e.ldo + col, g, buf[i * 32 + lane],
+                                 v4);
           }
           if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(e.upd.bad, 1u);
         } else if (raw) {
@@ -755,7 +775,7 @@ void launch_variant(const GemmPlan& p, cudaStream_t st) {
     std::lock_guard<std::mutex> lk(mu);
     if (!(configured >> dev & 1ull)) {
       LSGD_CUDA(cudaFuncSetAttribute(gemm_tf32x3_kernel<A_MN, B_MN, PAIR, EPI>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<PAIR, EPI>::SMEM));
       configured |= 1ull << dev;
     }
   }
@@ -765,7 +785,7 @@ void launch_variant(const GemmPlan& p, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.dynamicSmemBytes = Cfg<PAIR, EPI>::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;

@@ -296,30 +296,44 @@ __device__ __forceinline__ void store_split<float>(const UpdateArgs<float>& a, i
   }
 }
 
-template <typename T, bool EXACT>
+template <typename T, bool EXACT, int U>
 __global__ void __launch_bounds__(256) update_kernel(UpdateArgs<T> a) {
   constexpr int V = Vec<T>::kN;
   const int64_t nvec = a.scalar_only ? 0 : a.n_params / V;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   bool bad = false;
   const bool mom = a.mode != 0;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nvec; i += stride) {
-    const int64_t e = i * V;
-    const int64_t j = e / a.slice_len;  // slice_len is a multiple of V: a vector never straddles slices
-    Vec<T> d = ld16(a.slices.p[j] + (e - j * a.slice_len));
-    Vec<T> w = ld16(a.w + e), v;
-    if (mom) v = ld16(a.v + e);
+  // U vectors per thread per trip, all loads issued before the math (memory-level parallelism with few CTAs)
+  for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < nvec; i0 += U * stride) {
+    Vec<T> d[U], w[U], v[U];
 #pragma unroll
-    for (int q = 0; q < V; ++q) {
-      T dq = pre_delta(d.v[q], a);
-      T vq = mom ? v.v[q] : T(0);
-      sgd_one<T, EXACT>(w.v[q], vq, dq, a);
-      if (mom) v.v[q] = vq;
-      bad |= !isfinite(w.v[q]);
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < nvec) {
+        const int64_t e = i * V;
+        const int64_t j = e / a.slice_len;  // slice_len is a multiple of V: a vector never straddles slices
+        d[u] = ld16(a.slices.p[j] + (e - j * a.slice_len));
+        w[u] = ld16(a.w + e);
+        if (mom) v[u] = ld16(a.v + e);
+      }
     }
-    st16(a.w + e, w);
-    if (mom) st16(a.v + e, v);
-    store_split<T>(a, e, w.v, V);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= nvec) continue;
+      const int64_t e = i * V;
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        T dq = pre_delta(d[u].v[q], a);
+        T vq = mom ? v[u].v[q] : T(0);
+        sgd_one<T, EXACT>(w[u].v[q], vq, dq, a);
+        if (mom) v[u].v[q] = vq;
+        bad |= !isfinite(w[u].v[q]);
+      }
+      st16(a.w + e, w[u]);
+      if (mom) st16(a.v + e, v[u]);
+      store_split<T>(a, e, w[u].v, V);
+    }
   }
   const int64_t end = a.n_params + (a.loss_out ? 1 : 0);
   for (int64_t e = nvec * V + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < end; e += stride) {
@@ -573,15 +587,29 @@ void launch_update(const UpdateArgs<T>& a_in, bool exact, cudaStream_t st, Launc
   bool slices_ok = a.slice_len % Vec<T>::kN == 0;
   for (int j = 0; j < kMaxPeers && a.slices.p[j]; ++j) slices_ok = slices_ok && !misaligned(a.slices.p[j]);
   a.scalar_only = (misaligned(a.w) || misaligned(a.v) || misaligned(a.w_hi) || misaligned(a.w_lo) || !slices_ok) ? 1 : 0;
-  int64_t work = a.scalar_only ? a.n_params + 1 : a.n_params / Vec<T>::kN + 1;
+  static const int unroll = [] {
+    const char* e = std::getenv("LSGD_B200_UPD_UNROLL");
+    const int v = e ? std::atoi(e) : 1;
+    return (v == 2 || v == 4) ? v : 1;
+  }();
+  int64_t work = a.scalar_only ? a.n_params + 1 : a.n_params / Vec<T>::kN / unroll + 1;
   static const int cap = [] {
     const char* e = std::getenv("LSGD_B200_UPD_CTAS");
     const int v = e ? std::atoi(e) : 148 * 8;
     return v > 0 ? v : 148 * 8;
   }();
   int g = grid_for(work, 256, cap);
-  if (exact) update_kernel<T, true><<<g, 256, 0, st>>>(a);
-  else update_kernel<T, false><<<g, 256, 0, st>>>(a);
+#define LSGD_UPD(X, UU) update_kernel<T, X, UU><<<g, 256, 0, st>>>(a)
+  if (exact) {
+    if (unroll == 1) LSGD_UPD(true, 1);
+    else if (unroll == 4) LSGD_UPD(true, 4);
+    else LSGD_UPD(true, 2);
+  } else {
+    if (unroll == 1) LSGD_UPD(false, 1);
+    else if (unroll == 4) LSGD_UPD(false, 4);
+    else LSGD_UPD(false, 2);
+  }
+#undef LSGD_UPD
   ++lc.n;
   LSGD_CUDA(cudaGetLastError());
 }
