@@ -139,12 +139,15 @@ def cpu_reference(cfg_name: str, n: int, steps: int, warmup: int, bloc: int | No
     ref = Oracle("reference")
     if cfg_name == "cfg3":
         # OpenMP gradient scratch is min(32, B) x P doubles (mlp.cpp:243-245): keep B_loc small, dataset small
-        b = max(1, min(8, cores // max(1, n)))
+        # bounded sample (~10-60 s of CPU work whatever --steps is): a few iterations at a small per-worker batch;
+        # the reference's per-sample cost does not depend on the batch or dataset size
+        b = max(1, min(4, cores // max(1, n)))
+        iters = max(1, min(steps, 3))
         spec = TrainSpec(algorithm=algo, n_workers=n, n_groups=min(2, n) if algo == "lsgd" else 1,
                          layer_sizes=[4096, 8192, 8192, 512], n_samples=max(1024, 4 * b * n), n_features=4096,
-                         n_classes=512, mode="momentum", local_batch=b, iterations=steps)
+                         n_classes=512, mode="momentum", local_batch=b, iterations=iters)
         sample = (f"run_train lsgd {spec.n_groups}x{n // spec.n_groups}, MLP 4096-8192-8192-512 fp64, B_loc={b}, "
-                  f"{steps} iterations on {spec.n_samples} blobs (per-step cost is independent of n)")
+                  f"{iters} iterations on {spec.n_samples} blobs (per-step cost is independent of n)")
     else:
         b = bloc or 16
         spec = TrainSpec(algorithm=algo, n_workers=n, n_groups=min(2, n) if algo == "lsgd" else 1,
