@@ -141,7 +141,7 @@ def cpu_reference(cfg_name: str, n: int, steps: int, warmup: int, bloc: int | No
         # OpenMP gradient scratch is min(32, B) x P doubles (mlp.cpp:243-245): keep B_loc small, dataset small
         # bounded sample (~10-60 s of CPU work whatever --steps is): a few iterations at a small per-worker batch;
         # the reference's per-sample cost does not depend on the batch or dataset size
-        b = max(1, min(4, cores // max(1, n)))
+        b = max(1, min(8, cores // max(1, n)))
         iters = max(1, min(steps, 3))
         spec = TrainSpec(algorithm=algo, n_workers=n, n_groups=min(2, n) if algo == "lsgd" else 1,
                          layer_sizes=[4096, 8192, 8192, 512], n_samples=max(1024, 4 * b * n), n_features=4096,

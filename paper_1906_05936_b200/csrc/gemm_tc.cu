@@ -631,17 +631,29 @@ __global__ void softmax_xent_split_kernel(const float* __restrict__ logits, cons
 // partials combined in a fixed order (deterministic, no atomics).
 __global__ void bias_grad_f32_kernel(const float* __restrict__ delta, int b, int n, float* __restrict__ db,
                                      const __grid_constant__ BucketScatter scat, const __grid_constant__ FusedUpdate upd) {
-  __shared__ float part[8][33];
+  // 32 columns x 32 row partitions per block (each thread: rows y, y+32, ..., 4 loads in flight per trip), the
+  // partials combined in a fixed order: deterministic, no atomics
+  __shared__ float part[32][33];
   const int j = blockIdx.x * 32 + threadIdx.x;
   float acc = 0.f;
-  if (j < n)
-    for (int r = threadIdx.y; r < b; r += 8) acc += delta[static_cast<int64_t>(r) * n + j];
+  if (j < n) {
+    int r = threadIdx.y;
+    for (; r + 96 < b; r += 128) {
+      const float a0 = delta[static_cast<int64_t>(r) * n + j], a1 = delta[static_cast<int64_t>(r + 32) * n + j];
+      const float a2 = delta[static_cast<int64_t>(r + 64) * n + j], a3 = delta[static_cast<int64_t>(r + 96) * n + j];
+      acc += a0;
+      acc += a1;
+      acc += a2;
+      acc += a3;
+    }
+    for (; r < b; r += 32) acc += delta[static_cast<int64_t>(r) * n + j];
+  }
   part[threadIdx.y][threadIdx.x] = acc;
   __syncthreads();
   if (threadIdx.y == 0 && j < n) {
     float t = part[0][threadIdx.x];
 #pragma unroll
-    for (int q = 1; q < 8; ++q) t += part[q][threadIdx.x];
+    for (int q = 1; q < 32; ++q) t += part[q][threadIdx.x];
     t = __fdiv_rn(t, static_cast<float>(b));
     if (upd.w) {
       float d = t;
@@ -1010,6 +1022,31 @@ void tc_split_weights(TcWorkspace& ws, const Layout& L, const float* w, cudaStre
   split(w, L.n_params, ws.w_hi, ws.w_lo, st, lc);
 }
 
+// Gather of the shard rows straight into the TF32 split the first GEMM reads (x in fp32 is never materialised).
+__global__ void gather_split_kernel(const float* __restrict__ rows, const int32_t* __restrict__ labels,
+                                    const int32_t* __restrict__ idx, int d, float* __restrict__ hi,
+                                    float* __restrict__ lo, int32_t* __restrict__ y) {
+  const int s = blockIdx.x;
+  const int64_t r = idx[s];
+  if (threadIdx.x == 0) y[s] = labels[r];
+  const float4* src = reinterpret_cast<const float4*>(rows + r * d);
+  float4* h4 = reinterpret_cast<float4*>(hi + static_cast<int64_t>(s) * d);
+  float4* l4 = reinterpret_cast<float4*>(lo + static_cast<int64_t>(s) * d);
+  for (int i = threadIdx.x; i < d / 4; i += blockDim.x) {
+    const float4 v = src[i];
+    const float4 h = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+    h4[i] = h;
+    l4[i] = make_float4(tf32_rna(v.x - h.x), tf32_rna(v.y - h.y), tf32_rna(v.z - h.z), tf32_rna(v.w - h.w));
+  }
+}
+
+void tc_gather_split(TcWorkspace& ws, const Layout& L, const float* rows, const int32_t* labels, const int32_t* idx,
+                     int32_t* y, cudaStream_t st, LaunchCounter& lc) {
+  gather_split_kernel<<<ws.batch, 256, 0, st>>>(rows, labels, idx, L.in(0), ws.x_hi, ws.x_lo, y);
+  ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
+}
+
 void tc_split_input(TcWorkspace& ws, const Layout& L, const float* x, cudaStream_t st, LaunchCounter& lc) {
   split(x, static_cast<int64_t>(ws.batch) * L.in(0), ws.x_hi, ws.x_lo, st, lc);
 }
@@ -1063,7 +1100,7 @@ void tc_backward_bias(TcWorkspace& ws, const Layout& L, int k, float* gb, cudaSt
   const size_t di = static_cast<size_t>(k);
   BucketScatter sc = scat ? *scat : BucketScatter{};
   FusedUpdate fu = upd ? *upd : FusedUpdate{};
-  bias_grad_f32_kernel<<<(L.out(k) + 31) / 32, dim3(32, 8), 0, st>>>(ws.dlt[di], ws.batch, L.out(k), gb, sc, fu);
+  bias_grad_f32_kernel<<<(L.out(k) + 31) / 32, dim3(32, 32), 0, st>>>(ws.dlt[di], ws.batch, L.out(k), gb, sc, fu);
   ++lc.n;
   LSGD_CUDA(cudaGetLastError());
 }

@@ -41,6 +41,9 @@ void tc_alloc(TcWorkspace& ws, const Layout& L, int batch, int n_features);
 void tc_free(TcWorkspace& ws);
 // w -> (w_hi, w_lo) for the whole parameter vector (initial parameters; afterwards the fused update writes it).
 void tc_split_weights(TcWorkspace& ws, const Layout& L, const float* w, cudaStream_t st, LaunchCounter& lc);
+// Gather of the batch rows (dataset in HBM) straight into (x_hi, x_lo) + labels; d % 4 == 0.
+void tc_gather_split(TcWorkspace& ws, const Layout& L, const float* rows, const int32_t* labels, const int32_t* idx,
+                     int32_t* y, cudaStream_t st, LaunchCounter& lc);
 // Gathered batch x -> (x_hi, x_lo), the operand of the first forward GEMM.
 void tc_split_input(TcWorkspace& ws, const Layout& L, const float* x, cudaStream_t st, LaunchCounter& lc);
 // Forward layer k: act_k = ReLU?(in . W_k^T + b_k) and its split.

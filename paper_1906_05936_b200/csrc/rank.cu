@@ -514,6 +514,7 @@ class RankImpl final : public Rank {
     T* sample_loss = nullptr;
     T* loss_hist = nullptr;
     TcWorkspace tc;  // split-TF32 operands of the tensor-core path
+    bool x_split_ready = false;  // io() gathered this step's rows straight into the TC split
     const PeerLayout* lay = nullptr;
     int64_t Sg = 0;
     T* blk_stage(int m) const { return reinterpret_cast<T*>(blk + lay->stage) + static_cast<int64_t>(m) * Sg; }
@@ -745,7 +746,12 @@ class RankImpl final : public Rank {
       LSGD_CUDA(cudaMemcpyAsync(w.idx, dst + i * B_, sizeof(int32_t) * B_, cudaMemcpyHostToDevice, main_));
       {
         Timed tm(this, "gather", main_);
-        launch_gather<T>(data_x_, data_y_, w.idx, B_, spec_.c.n_features, w.x, w.y, main_, lc_);
+        if (use_tc_ && spec_.c.n_features % 4 == 0) {  // rows straight into the first GEMM's TF32 split
+          tc_gather_split(w.tc, L_, reinterpret_cast<const float*>(data_x_), data_y_, w.idx, w.y, main_, lc_);
+          w.x_split_ready = true;
+        } else {
+          launch_gather<T>(data_x_, data_y_, w.idx, B_, spec_.c.n_features, w.x, w.y, main_, lc_);
+        }
       }
       phase_mark(i, t, 0, 1, main_);
     }
@@ -760,10 +766,11 @@ class RankImpl final : public Rank {
   void forward_layer(Worker& w, int k) {
     if (synth_) return;
     if (use_tc_) {
-      if (k == 0) {
+      if (k == 0 && !w.x_split_ready) {
         Timed ts(this, "split", main_);
         tc_split_input(w.tc, L_, reinterpret_cast<const float*>(w.x), main_, lc_);
       }
+      if (k == 0) w.x_split_ready = false;
       Timed tm(this, "gemm", main_);
       tc_forward_layer(w.tc, L_, k, reinterpret_cast<const float*>(w.w), main_, lc_);
       return;
