@@ -321,6 +321,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                        const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
                        int k_per_split, int splits, const __grid_constant__ EpiParams ep) {
   using C = Cfg<PAIR, EPI>;
+  // tile order: m fastest (concurrent slots share B tiles in L2), except for the fused update, whose epilogue
+  // streams w / v / w_hi / w_lo rows: n fastest keeps concurrent tiles on the same rows (DRAM page locality)
+  constexpr bool kNFast = EPI == kWgradUpd;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -378,8 +381,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t it = 0;  // k-blocks issued by this CTA across all its tiles (stage ring position)
       for (int t = slot; t < tiles; t += nslots) {
         const int z = t / (mt * nt), r = t % (mt * nt);
-        const int m0 = (r % mt) * BM * PAIR + static_cast<int>(rank) * BM;
-        const int n0 = (r / mt) * BN + static_cast<int>(rank) * C::B_ROWS, k0 = z * k_per_split;
+        const int tm = kNFast ? r / nt : r % mt, tn = kNFast ? r % nt : r / mt;
+        const int m0 = tm * BM * PAIR + static_cast<int>(rank) * BM;
+        const int n0 = tn * BN + static_cast<int>(rank) * C::B_ROWS, k0 = z * k_per_split;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
           if (it >= STAGES) mbar_wait(&empty_bar[s], ph ^ 1u);
@@ -441,7 +445,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t local = 0;
     for (int t = slot; t < tiles; t += nslots, ++local) {
       const int z = t / (mt * nt), r = t % (mt * nt);
-      const int m0 = (r % mt) * BM * PAIR + static_cast<int>(rank) * BM, n0 = (r / mt) * BN;
+      const int tm = kNFast ? r / nt : r % mt, tn = kNFast ? r % nt : r / mt;
+      const int m0 = tm * BM * PAIR + static_cast<int>(rank) * BM, n0 = tn * BN;
       const uint32_t a = local & 1u;
       // scalar fields in registers; the scatter table stays in (grid-constant) param space, where it is indexed
       const EpiParams e = ep;
@@ -767,11 +772,20 @@ struct GemmPlan {
   EpiParams ep{};
 };
 
+// SMs the persistent GEMM may occupy (LSGD_TC_MAX_SMS caps it: the rest stay free for the update / exchange
+// kernels, which are kept off GEMM SMs by their shared-memory request; tuning knob)
 int sm_count() {
   static int sms = [] {
     int v = 0;
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, 0);
-    return v > 0 ? v : 148;
+    if (v <= 0) v = 148;
+    if (const char* e = std::getenv("LSGD_TC_MAX_SMS")) {
+      const int cap = std::atoi(e);
+        if (cap >= 2 && cap < v) v = cap;
+    } else if (v == 148) {
+      v = 128;  // 64 CTA pairs: every cfg3 GEMM has a multiple of 64 pair tiles, the other 20 SMs run side work
+    }
+    return v;
   }();
   return sms;
 }

@@ -51,6 +51,16 @@ __device__ __forceinline__ void st16(T* p, const Vec<T>& v) {
   *reinterpret_cast<Vec<T>*>(p) = v;
 }
 
+// Dynamic shared memory requested by the update / exchange kernels (LSGD_B200_SIDE_SMEM, bytes; unused by the
+// kernels): > 227 KB - the GEMM's 209 KB keeps them off SMs that hold a GEMM CTA (tuning knob).
+inline size_t side_smem() {
+  static const size_t n = [] {
+    const char* e = std::getenv("LSGD_B200_SIDE_SMEM");
+    return static_cast<size_t>(e ? std::atol(e) : 0);
+  }();
+  return n;
+}
+
 inline int grid_for(int64_t work, int threads, int cap = 148 * 8) {
   int64_t g = (work + threads - 1) / threads;
   if (g < 1) g = 1;
@@ -599,7 +609,7 @@ void launch_update(const UpdateArgs<T>& a_in, bool exact, cudaStream_t st, Launc
     return v > 0 ? v : 148 * 8;
   }();
   int g = grid_for(work, 256, cap);
-#define LSGD_UPD(X, UU) update_kernel<T, X, UU><<<g, 256, 0, st>>>(a)
+#define LSGD_UPD(X, UU) update_kernel<T, X, UU><<<g, 256, side_smem(), st>>>(a)
   if (exact) {
     if (unroll == 1) LSGD_UPD(true, 1);
     else if (unroll == 4) LSGD_UPD(true, 4);
@@ -654,10 +664,10 @@ void launch_reduce_push(SrcList<T> src, int n_src, int64_t len, DstList<T> dst, 
   constexpr int U = 4;
   const int g = grid_for(len / Vec<T>::kN / U + 1, 256, comm_ctas());
   switch (n_src) {
-    case 1: reduce_push_kernel<T, 1, U><<<g, 256, 0, st>>>(src, n_src, len, dst, n_dst, add_zero, divisor); break;
-    case 2: reduce_push_kernel<T, 2, U><<<g, 256, 0, st>>>(src, n_src, len, dst, n_dst, add_zero, divisor); break;
-    case 4: reduce_push_kernel<T, 4, U><<<g, 256, 0, st>>>(src, n_src, len, dst, n_dst, add_zero, divisor); break;
-    default: reduce_push_kernel<T, 0, U><<<g, 256, 0, st>>>(src, n_src, len, dst, n_dst, add_zero, divisor); break;
+    case 1: reduce_push_kernel<T, 1, U><<<g, 256, side_smem(), st>>>(src, n_src, len, dst, n_dst, add_zero, divisor); break;
+    case 2: reduce_push_kernel<T, 2, U><<<g, 256, side_smem(), st>>>(src, n_src, len, dst, n_dst, add_zero, divisor); break;
+    case 4: reduce_push_kernel<T, 4, U><<<g, 256, side_smem(), st>>>(src, n_src, len, dst, n_dst, add_zero, divisor); break;
+    default: reduce_push_kernel<T, 0, U><<<g, 256, side_smem(), st>>>(src, n_src, len, dst, n_dst, add_zero, divisor); break;
   }
   ++lc.n;
   LSGD_CUDA(cudaGetLastError());
@@ -666,7 +676,7 @@ void launch_reduce_push(SrcList<T> src, int n_src, int64_t len, DstList<T> dst, 
 template <typename T>
 void launch_copy_pairs(SrcList<T> src, DstList<T> dst, int n_pairs, int64_t len, cudaStream_t st, LaunchCounter& lc) {
   if (n_pairs == 0) return;
-  copy_pairs_kernel<T, 4><<<grid_for(len / Vec<T>::kN / 4 + 1, 256, comm_ctas()), 256, 0, st>>>(src, dst, n_pairs,
+  copy_pairs_kernel<T, 4><<<grid_for(len / Vec<T>::kN / 4 + 1, 256, comm_ctas()), 256, side_smem(), st>>>(src, dst, n_pairs,
                                                                                                   len);
   ++lc.n;
   LSGD_CUDA(cudaGetLastError());
