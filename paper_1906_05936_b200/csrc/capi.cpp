@@ -81,7 +81,7 @@ int lsgd_b200_config_init(lsgd_b200_config* c) {
     c->collective_timeout_s = 30.0;
     c->shared_minibatch = 1;
     c->dtype = LSGD_B200_FP32;
-    c->global_algo = LSGD_B200_GLOBAL_NCCL;
+    c->global_algo = LSGD_B200_GLOBAL_ORDERED;  // push exchange in the reference order (NCCL: opt-in)
     c->gemm = LSGD_B200_GEMM_AUTO;
     c->data_source = LSGD_B200_DATA_DEVICE;
     c->model = LSGD_B200_MODEL_MLP;

@@ -35,6 +35,7 @@ int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 struct PhaseEvents {
   cudaEvent_t ev[6][2];
   bool used[6];
+  bool marked[6][2];  // both ends recorded (a span that was never closed reads as absent, not as an error)
 };
 }  // namespace
 
@@ -373,7 +374,7 @@ class RankImpl final : public Rank {
       for (int p = 0; p < 6; ++p) {
         double b = 0, e = 0;
         if (wi < phase_ev_.size() && t < static_cast<int64_t>(phase_ev_[wi].size()) &&
-            phase_ev_[wi][static_cast<size_t>(t)].used[p]) {
+            phase_ev_[wi][static_cast<size_t>(t)].marked[p][0] && phase_ev_[wi][static_cast<size_t>(t)].marked[p][1]) {
           float ms0 = 0, ms1 = 0;
           LSGD_CUDA(cudaEventElapsedTime(&ms0, t0_ev_, phase_ev_[wi][static_cast<size_t>(t)].ev[p][0]));
           LSGD_CUDA(cudaEventElapsedTime(&ms1, t0_ev_, phase_ev_[wi][static_cast<size_t>(t)].ev[p][1]));
@@ -680,6 +681,7 @@ class RankImpl final : public Rank {
       pe.used[phase] = true;
     }
     LSGD_CUDA(cudaEventRecord(pe.ev[phase][end], st));
+    pe.marked[phase][end] = true;
   }
   size_t widx(const Worker& w) const { return static_cast<size_t>(&w - ws_.data()); }
 
@@ -1186,7 +1188,6 @@ class RankImpl final : public Rank {
         LSGD_NCCL(ncclAllReduce(w.payload, w.payload, static_cast<size_t>(geo_.Ppad), nccl_type(), ncclSum,
                                 flat_comm_, main_));
     } else if (exchange) {
-      for (auto& w : ws_) phase_mark(widx(w), t, 2, 0, comm_);
       if (split_) {
         Worker& w = ws_[0];
         // with the ordered push sum (no NCCL) consecutive buckets alternate between two streams so one bucket's
@@ -1197,7 +1198,11 @@ class RankImpl final : public Rank {
           cudaStream_t cs = (n_streams == 2 && (q & 1)) ? comm2_ : comm_;
           LSGD_CUDA(cudaStreamWaitEvent(cs, ev_bucket_[b], 0));
           if (q == 0) {
+            // phases (executors.hpp:85): the push exchange interleaves the local reduce and the global average per
+            // bucket, so local_reduce spans the whole exchange and global_allreduce starts after the link delay
+            phase_mark(widx(w), t, 2, 0, comm_);
             launch_sleep(spec_.c.global_link_delay_s, comm_, lc_);
+            phase_mark(widx(w), t, 3, 0, comm_);
             if (n_streams == 2) {  // the injected link delay precedes every bucket's exchange
               LSGD_CUDA(cudaEventRecord(join_ev_, comm_));
               LSGD_CUDA(cudaStreamWaitEvent(comm2_, join_ev_, 0));
@@ -1205,16 +1210,25 @@ class RankImpl final : public Rank {
           }
           exchange_push_bucket(w, b, t, cs);
         }
+        if (spec_.c.record_phases && n_streams == 2) {  // both streams' work closes the spans
+          LSGD_CUDA(cudaEventRecord(join_ev_, comm2_));
+          LSGD_CUDA(cudaStreamWaitEvent(comm_, join_ev_, 0));
+        }
+        phase_mark(widx(w), t, 2, 1, comm_);
+        phase_mark(widx(w), t, 3, 1, comm_);
       } else {
         // emulated ranks share one stream: every local slice sum is published before any global average waits
+        for (auto& w : ws_) phase_mark(widx(w), t, 2, 0, main_);
         for (int b : order)
           for (auto& w : ws_) reduce_bucket(w, b, t, main_);
+        for (auto& w : ws_) phase_mark(widx(w), t, 2, 1, main_);
         current_phase() = "global_allreduce";
+        for (auto& w : ws_) phase_mark(widx(w), t, 3, 0, main_);
         launch_sleep(spec_.c.global_link_delay_s, main_, lc_);
         for (int b : order)
           for (auto& w : ws_) global_bucket(w, b, t, main_);
+        for (auto& w : ws_) phase_mark(widx(w), t, 3, 1, main_);
       }
-      for (auto& w : ws_) phase_mark(widx(w), t, 3, 1, comm_);
     }
 
     // Eager update of round t on the update stream, in backward order. Host issue order matters: these may spin on

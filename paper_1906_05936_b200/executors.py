@@ -25,7 +25,7 @@ class B200Options:
 
     dtype: str = "fp32"              # fp32 | fp64 (parity mode)
     n_devices: int = 0               # 0: min(visible GPUs, n_workers)
-    global_allreduce: str = "nccl"   # nccl | ordered
+    global_allreduce: str = "ordered"   # ordered (reference order, push exchange) | nccl
     gemm: str = "auto"               # auto | simt | tcgen05
     data: str = "device"             # device | host
     model: str = "mlp"               # mlp | synthetic_gradient

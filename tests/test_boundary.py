@@ -14,6 +14,7 @@ from paper_1906_05936_b200 import host
 from paper_1906_05936_b200.config import parse_run_config
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF_INCLUDE = "/root/reference/proj/include/lsgd"  # present in the build container only (CPU tests)
 GOLD = os.path.join(ROOT, "tests", "golden")
 REFT = json.load(open(os.path.join(GOLD, "reference_tests.json")))
 FX = np.load(os.path.join(GOLD, "ref_fixtures.npz"))
@@ -152,3 +153,33 @@ def test_compute_entry_points_fail_loudly_without_gpu():
     cfg = lsgd.TrainConfig(algorithm="sequential", iterations=1)
     with pytest.raises(lsgd.LsgdError):
         lsgd.run_train(cfg)
+
+
+def test_metrics_csv_schema_matches_the_reference(tmp_path):
+    """metrics.cpp:32-44 / metrics.hpp:12-15: exact header, one row per iteration, %.17g, the global allreduce
+    attributed to the widest owner span (executors.cpp:343-353)."""
+    import numpy as np
+    from paper_1906_05936_b200.executors import TrainResult
+    ref_header = open(os.path.join(REF_INCLUDE, "metrics.hpp")).read() if os.path.isdir(REF_INCLUDE) else None
+    cfg = lsgd.TrainConfig(algorithm="lsgd", n_workers=2, n_groups=2, layer_sizes=[4, 3], n_samples=100,
+                           local_batch=5, iterations=2)
+    spans = np.zeros((2, 2, 6, 2))
+    for t in range(2):
+        for p in range(6):
+            spans[:, t, p] = [t + 0.1 * p, t + 0.1 * p + 0.05]
+    spans[1, 1, 3] = [1.3, 1.5]  # worker 1's global allreduce of round 1 is the widest
+    res = TrainResult(np.zeros(15), np.zeros(15), np.array([2.0, 1.5]), np.array([0.1, 0.1]), None, np.zeros((2, 15)),
+                      np.zeros((2, 2), dtype=np.int64), spans, 1.0, 20.0, 0)
+    path = tmp_path / "m.csv"
+    lsgd.write_metrics_csv(str(path), "r1", cfg, res)
+    lines = path.read_text().splitlines()
+    assert lines[0] == lsgd.K_METRICS_HEADER
+    if ref_header is not None:
+        flat = "".join(x.strip().strip('"') for x in ref_header.split("kMetricsHeader =")[1].split(";")[0].split("\n"))
+        assert flat == lsgd.K_METRICS_HEADER
+    assert len(lines) == 3
+    row = lines[2].split(",")
+    assert row[:5] == ["r1", "lsgd", "2", "2", "1"]
+    assert float(row[5]) == 1 * 10 / 100  # epoch = t * global_batch / n
+    assert abs(float(row[11]) - 0.2) < 1e-12  # widest global allreduce span
+    assert abs(float(row[8]) - 0.05) < 1e-12 and abs(float(row[14]) - 0.55) < 1e-12

@@ -281,3 +281,34 @@ def test_row_block_buckets_keep_parity(dtype, tol, monkeypatch):
     ref = Oracle("port").run_train(spec, history=True)["history"]
     e = compare_histories(ref, r.param_history, "blocks")
     assert (e.max_rel_deviation if dtype == "fp64" else e.max_normwise_deviation) <= tol, e
+
+
+@pytest.mark.parametrize("n_devices", [1, 4])
+def test_phase_spans_and_io_overlaps_global_allreduce(n_devices, n_gpus, tmp_path):
+    """test_executors.cpp:195-220 on the GPU: with injected io (20 ms) and link (12 ms) delays LSGD's mean block is
+    shorter than CSGD's, and worker 0's io of block t+1 overlaps the global allreduce of round t. The recorded spans
+    feed the reference-schema metrics CSV (metrics.cpp:32-44)."""
+    if n_gpus < n_devices:
+        pytest.skip(f"needs {n_devices} GPUs")
+    res = {}
+    for alg, G in (("csgd", 1), ("lsgd", 2)):
+        cfg = lsgd.TrainConfig(algorithm=alg, n_workers=4, n_groups=G, layer_sizes=[16, 8, 4], n_samples=512,
+                               n_features=16, n_classes=4, spread=6.0, local_batch=8, iterations=8,
+                               io_delay_s=0.020, global_link_delay_s=0.012)
+        cfg.b200.n_devices = n_devices
+        cfg.b200.record_phases = True
+        res[alg] = (cfg, lsgd.run_train(cfg))
+    if n_devices > 1:  # one worker per GPU: the exchange runs on its own streams, concurrently with the next io
+        assert res["lsgd"][1].total_wall_s < res["csgd"][1].total_wall_s
+        sp = res["lsgd"][1].phase_spans
+        for t in range(7):
+            io_next, ar = sp[0, t + 1, 0], sp[:, t, 3]
+            assert io_next[1] > io_next[0]
+            assert any(a[1] > a[0] and a[0] < io_next[1] and io_next[0] < a[1] for a in ar), (t, io_next, ar)
+    cfg, r = res["lsgd"]
+    path = tmp_path / "metrics.csv"
+    lsgd.write_metrics_csv(str(path), "gpu", cfg, r)
+    rows = path.read_text().splitlines()
+    assert rows[0] == lsgd.K_METRICS_HEADER and len(rows) == 9
+    io_s = np.array([float(x.split(",")[8]) for x in rows[1:]])
+    assert np.all(io_s > 0.015)  # the injected 20 ms io delay shows up in t_io_s
