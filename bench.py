@@ -328,6 +328,18 @@ def run_b200_arm(args):
             peak = peaks.get("hbm_gbs") or 6650.0
             roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": (ach / peak) if ach else None,
                     "traffic": None, "kernel": "K8 broadcast-pull + momentum update"}
+        # step-level roofline of the north star: t_roof = max(B_loc*F / GEMM_peak,
+        # 4(P+1) / BW_NVLink), GEMM_peak = the 3xTF32 effective rate of the measured dense peak (peak/6)
+        step_roof = None
+        if cfg.b200.model == "mlp":
+            gemm_peak = (peaks.get("bf16_tflops_sustained") or 1400.0) / 6.0 * 1e12
+            t_gemm = B * flops_per_sample(cfg.layer_sizes) / gemm_peak
+            t_link = 4.0 * (cfg.n_params + 1) / 900e9 if n > 1 else 0.0
+            t_roof = max(t_gemm, t_link)
+            step_roof = {"t_roof_ms": t_roof * 1e3, "t_step_ms": ms_max / args.steps,
+                         "frac": t_roof * 1e3 / (ms_max / args.steps), "t_gemm_ms": t_gemm * 1e3,
+                         "t_nvlink_ms": t_link * 1e3,
+                         "basis": "3xTF32 = bf16_tflops_sustained/6; NVLink 900 GB/s per direction"}
         kern = {f: {"avg_ms": v[0], "count": v[1], "ms_per_step": v[0] * v[1] / args.steps}
                 for f, v in fams.items() if v[1]}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
@@ -340,7 +352,7 @@ def run_b200_arm(args):
                            "global_allreduce": cfg.b200.global_allreduce,
                            "l2": "working set (w, v, grad, slices) >> 126 MB L2; no flush needed"},
                 "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,
-                "kernels": kern, "setup_s": setup_s}
+                "step_roofline": step_roof, "kernels": kern, "setup_s": setup_s}
         print(json.dumps(line), flush=True)
     r.close()
     if pg:
