@@ -601,6 +601,16 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, int64_t n, float*
   }
 }
 
+// Mean of the per-sample losses for the fp32 path: one warp, lanes own a fixed strided subset, fixed shuffle tree
+// (deterministic; the fp64 parity path keeps the reference's sequential fold, mlp.cpp:262-271).
+__global__ void mean_loss_warp_kernel(const float* __restrict__ sample_loss, int b, float* __restrict__ out) {
+  float acc = 0.f;
+  for (int s = threadIdx.x; s < b; s += 32) acc += sample_loss[s];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (threadIdx.x == 0) *out = __fdiv_rn(acc, static_cast<float>(b));
+}
+
 // Softmax-CE head for the tensor-core path: one warp per sample, lanes striding the classes (coalesced), max and
 // sum by warp shuffles; writes delta = softmax - onehot and its hi/lo split for the backward GEMMs.
 __global__ void softmax_xent_split_kernel(const float* __restrict__ logits, const int32_t* __restrict__ labels, int b,
@@ -610,6 +620,44 @@ __global__ void softmax_xent_split_kernel(const float* __restrict__ logits, cons
   const int lane = threadIdx.x % 32;
   if (s >= b) return;
   const float* z = logits + static_cast<int64_t>(s) * c;
+  const int lab = labels[s];
+  if (c <= 32 * 32) {  // the sample's logits stay in registers (one global read instead of three)
+    float zr[32];
+    float zmax = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int k = lane + 32 * q;
+      zr[q] = k < c ? z[k] : -INFINITY;
+      zmax = fmaxf(zmax, zr[q]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) zmax = fmaxf(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
+    float sum = 0.f;
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      if (lane + 32 * q < c) sum += expf(zr[q] - zmax);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float lse = zmax + logf(sum);
+    float zl = 0.f;  // the label's logit, selected without dynamic register indexing
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      if (q == lab / 32) zl = zr[q];
+    if (lane == lab % 32) sample_loss[s] = lse - zl;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int k = lane + 32 * q;
+      if (k >= c) break;
+      const float p = expf(zr[q] - lse);
+      const float d = (k == lab) ? p - 1.f : p;
+      const int64_t at = static_cast<int64_t>(s) * c + k;
+      delta[at] = d;
+      const float h = tf32_rna(d);
+      dhi[at] = h;
+      dlo[at] = tf32_rna(d - h);
+    }
+    return;
+  }
   float zmax = -INFINITY;
   for (int k = lane; k < c; k += 32) zmax = fmaxf(zmax, z[k]);
 #pragma unroll
@@ -619,7 +667,6 @@ __global__ void softmax_xent_split_kernel(const float* __restrict__ logits, cons
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
   const float lse = zmax + logf(sum);
-  const int lab = labels[s];
   if (lane == 0) sample_loss[s] = lse - z[lab];
   for (int k = lane; k < c; k += 32) {
     const float p = expf(z[k] - lse);
@@ -1046,6 +1093,7 @@ __global__ void gather_split_kernel(const float* __restrict__ rows, const int32_
   const float4* src = reinterpret_cast<const float4*>(rows + r * d);
   float4* h4 = reinterpret_cast<float4*>(hi + static_cast<int64_t>(s) * d);
   float4* l4 = reinterpret_cast<float4*>(lo + static_cast<int64_t>(s) * d);
+#pragma unroll 4
   for (int i = threadIdx.x; i < d / 4; i += blockDim.x) {
     const float4 v = src[i];
     const float4 h = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
@@ -1081,7 +1129,9 @@ void tc_head(TcWorkspace& ws, const Layout& L, const int32_t* y, float* sample_l
                                                              ws.dlt[top], ws.dlt_hi[top], ws.dlt_lo[top], sample_loss);
   ++lc.n;
   LSGD_CUDA(cudaGetLastError());
-  launch_mean_loss<float>(sample_loss, B, loss_out, st, lc);
+  mean_loss_warp_kernel<<<1, 32, 0, st>>>(sample_loss, B, loss_out);
+  ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
 }
 
 void tc_backward_dw(TcWorkspace& ws, const Layout& L, int k, int row0, int rows, float* gW, cudaStream_t st,
