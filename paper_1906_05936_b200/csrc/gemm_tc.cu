@@ -37,13 +37,16 @@ constexpr int EPI_STAGE_BYTES = 32 * 32 * 4;  // per epilogue warp: one 32 x 32 
 // fused update: per epilogue warp, w and v of one 32 x 32 chunk (8 KB), double-buffered (cp.async one chunk ahead)
 constexpr int UPD_PREF_BYTES = 2 * 2 * EPI_STAGE_BYTES;
 enum : int { kFwd = 0, kWgrad = 1, kIgrad = 2, kRaw = 3, kWgradUpd = 4 };  // kWgradUpd: dW + fused update
-template <int PAIR, int EPI = kFwd>
+template <int PAIR, int EPI = kFwd, bool WS = false>
 struct Cfg {
   static constexpr int B_ROWS = BN / PAIR;                          // B rows staged by one CTA
   static constexpr int B_BYTES = B_ROWS * BK * 4;                   // 16 KB | 8 KB
-  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;     // 48 KB | 32 KB (hi + lo of both operands)
+  // WS: B (the weights) arrives as raw fp32 and is split into hi / lo in shared memory (no w_hi / w_lo in HBM)
+  static constexpr int RAW_BYTES = WS ? B_BYTES : 0;
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES + RAW_BYTES;  // 48 | 32 KB (+16 | 8 KB raw)
   // the fused-update epilogue trades mainloop stages (K = B is short) for its w/v staging
-  static constexpr int STAGES = EPI == kWgradUpd ? (PAIR == 2 ? 4 : 3) : STAGE_RING_BYTES / STAGE_BYTES;  // 4 | 6
+  static constexpr int STAGES = EPI == kWgradUpd ? (PAIR == 2 ? 4 : 3)
+                                : (WS ? (208 * 1024) / STAGE_BYTES : STAGE_RING_BYTES / STAGE_BYTES);  // 4 | 6 (WS: 3 | 5)
   static constexpr int RING = STAGES * STAGE_BYTES;
   static constexpr int PREF = EPI == kWgradUpd ? 4 * UPD_PREF_BYTES : 0;
   static constexpr int SMEM = RING + 4 * EPI_STAGE_BYTES + PREF + 1024;  // + alignment slack
@@ -141,6 +144,14 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
+}
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(smem_dst)), "l"(gmem_src) : "memory");
@@ -315,12 +326,12 @@ __device__ __forceinline__ void epi_vec4(const EpiParams& ep, int row, int col, 
 // (2 x 256 columns) let the epilogue of tile i overlap the MMAs of tile i+1; the smem stage ring runs continuously
 // across tiles. In pair mode the leader CTA (rank 0) issues the cta_group::2 MMAs and owns the full/tmem-empty
 // barriers; both CTAs load their halves, and the MMA commits multicast to both CTAs' empty/tmem-full barriers.
-template <bool A_MN, bool B_MN, int PAIR, int EPI>
+template <bool A_MN, bool B_MN, int PAIR, int EPI, bool WS>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                        const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
                        int k_per_split, int splits, const __grid_constant__ EpiParams ep) {
-  using C = Cfg<PAIR, EPI>;
+  using C = Cfg<PAIR, EPI, WS>;
   // tile order: m fastest (concurrent slots share B tiles in L2), except for the fused update, whose epilogue
   // streams w / v / w_hi / w_lo rows: n fastest keeps concurrent tiles on the same rows (DRAM page locality)
   constexpr bool kNFast = EPI == kWgradUpd;
@@ -331,6 +342,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __shared__ alignas(8) uint64_t empty_bar[STAGES];
   __shared__ alignas(8) uint64_t tfull_bar[2];
   __shared__ alignas(8) uint64_t tempty_bar[2];
+  __shared__ alignas(8) uint64_t xform_bar[WS ? STAGES : 1];  // WS: stage s split into hi / lo (both CTAs)
   __shared__ uint32_t tmem_slot;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -349,6 +361,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], 4 * PAIR);  // one arrival per epilogue warp of each CTA
     }
+    if (WS)
+      for (int s = 0; s < STAGES; ++s) mbar_init(&xform_bar[s], 4 * PAIR);  // one per transform warp per CTA
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (ep.prefetch) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta_hi)) : "memory");
@@ -392,8 +406,17 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (rank == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full_bar[s])) : "memory");
             continue;
           }
-          if (rank == 0) mbar_expect_tx(&full_bar[s], C::STAGE_BYTES * PAIR);  // the leader counts both halves
           const int k = k0 + kb * BK;
+          if (WS) {
+            // every CTA completes its own barrier (its transform warps wait on it); the raw weights land behind
+            // the hi / lo slots the transform fills
+            mbar_expect_tx(&full_bar[s], 2 * A_BYTES + C::RAW_BYTES);
+            load_op<A_MN, 1>(&ta_hi, &full_bar[s], st, m0, k);
+            load_op<A_MN, 1>(&ta_lo, &full_bar[s], st + A_BYTES, m0, k);
+            load_op<B_MN, 1>(&tb_hi, &full_bar[s], st + 2 * A_BYTES + 2 * C::B_BYTES, n0, k);
+            continue;
+          }
+          if (rank == 0) mbar_expect_tx(&full_bar[s], C::STAGE_BYTES * PAIR);  // the leader counts both halves
           load_op<A_MN, PAIR>(&ta_hi, &full_bar[s], st, m0, k);
           load_op<A_MN, PAIR>(&ta_lo, &full_bar[s], st + A_BYTES, m0, k);
           load_op<B_MN, PAIR>(&tb_hi, &full_bar[s], st + 2 * A_BYTES, n0, k);
@@ -412,7 +435,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t acc_tmem = tmem + a * TMEM_COLS;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
-          mbar_wait(&full_bar[s], ph);
+          mbar_wait(WS ? &xform_bar[s] : &full_bar[s], ph);
           tc_fence_after();
           const uint32_t st = su32(smem + s * C::STAGE_BYTES);
           const uint32_t a_hi = st, a_lo = st + A_BYTES, b_hi = st + 2 * A_BYTES, b_lo = b_hi + C::B_BYTES;
@@ -443,7 +466,38 @@ __global__ void __launch_bounds__(THREADS, 1)
     // epilogue warps 2..5 -> TMEM lane quadrant warp % 4 (this CTA's 128 rows of the tile)
     const int q = warp & 3;
     uint32_t local = 0;
+    uint32_t xit = 0;  // WS: k-blocks transformed (same stage ring position as producer / MMA)
     for (int t = slot; t < tiles; t += nslots, ++local) {
+      if (WS) {
+        // split this tile's raw weight tiles into the hi / lo operand slots as they land: elementwise, so the
+        // TMA swizzle (a 16 B-chunk permutation shared by all three tiles) needs no index math
+        const int tid = threadIdx.x - 64;
+        for (int kb = 0; kb < nkb; ++kb, ++xit) {
+          const uint32_t s = xit % STAGES, ph = (xit / STAGES) & 1u;
+          mbar_wait(&full_bar[s], ph);
+          uint8_t* st = smem + s * C::STAGE_BYTES;
+          const uint32_t raw = su32(st + 2 * A_BYTES + 2 * C::B_BYTES);
+          const uint32_t hi = su32(st + 2 * A_BYTES), lo = su32(st + 2 * A_BYTES + C::B_BYTES);
+          constexpr int N4 = C::B_BYTES / 16;
+          float4 v[N4 / 128];
+#pragma unroll
+          for (int j = 0; j < N4 / 128; ++j) v[j] = lds128(raw + 16u * (tid + 128 * j));  // all loads first
+#pragma unroll
+          for (int j = 0; j < N4 / 128; ++j) {
+            const uint32_t o = 16u * (tid + 128 * j);
+            const float4 h = make_float4(tf32_rna(v[j].x), tf32_rna(v[j].y), tf32_rna(v[j].z), tf32_rna(v[j].w));
+            sts128(hi + o, h);
+            sts128(lo + o, make_float4(tf32_rna(v[j].x - h.x), tf32_rna(v[j].y - h.y), tf32_rna(v[j].z - h.z),
+                                       tf32_rna(v[j].w - h.w)));
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
+          __syncwarp();
+          if (lane == 0) {
+            const uint32_t bar = PAIR == 2 ? (su32(&xform_bar[s]) & kPeerMask) : su32(&xform_bar[s]);
+            asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+          }
+        }
+      }
       const int z = t / (mt * nt), r = t % (mt * nt);
       const int tm = kNFast ? r / nt : r % mt, tn = kNFast ? r % nt : r / mt;
       const int m0 = tm * BM * PAIR + static_cast<int>(rank) * BM, n0 = tn * BN;
@@ -813,8 +867,8 @@ CUtensorMap make_map(const OpView& v, int tile_rows) {
 }
 
 struct GemmPlan {
-  CUtensorMap a_hi, a_lo, b_hi, b_lo;
-  bool a_mn = false, b_mn = false;
+  CUtensorMap a_hi, a_lo, b_hi, b_lo;  // ws: b_hi maps the raw fp32 weights (b_lo unused)
+  bool a_mn = false, b_mn = false, ws = false;
   int M = 0, N = 0, K = 0, splits = 1, epi = 0, pair = 1;
   EpiParams ep{};
 };
@@ -837,7 +891,7 @@ int sm_count() {
   return sms;
 }
 
-template <bool A_MN, bool B_MN, int PAIR, int EPI>
+template <bool A_MN, bool B_MN, int PAIR, int EPI, bool WS = false>
 void launch_variant(const GemmPlan& p, cudaStream_t st) {
   // the dynamic-smem opt-in is per device: remember which devices this instantiation was configured on
   static std::mutex mu;
@@ -847,8 +901,8 @@ void launch_variant(const GemmPlan& p, cudaStream_t st) {
   {
     std::lock_guard<std::mutex> lk(mu);
     if (!(configured >> dev & 1ull)) {
-      LSGD_CUDA(cudaFuncSetAttribute(gemm_tf32x3_kernel<A_MN, B_MN, PAIR, EPI>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<PAIR, EPI>::SMEM));
+      LSGD_CUDA(cudaFuncSetAttribute(gemm_tf32x3_kernel<A_MN, B_MN, PAIR, EPI, WS>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<PAIR, EPI, WS>::SMEM));
       configured |= 1ull << dev;
     }
   }
@@ -858,7 +912,7 @@ void launch_variant(const GemmPlan& p, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = Cfg<PAIR, EPI>::SMEM;
+  cfg.dynamicSmemBytes = Cfg<PAIR, EPI, WS>::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -867,7 +921,7 @@ void launch_variant(const GemmPlan& p, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  LSGD_CUDA(cudaLaunchKernelEx(&cfg, gemm_tf32x3_kernel<A_MN, B_MN, PAIR, EPI>, p.a_hi, p.a_lo, p.b_hi, p.b_lo,
+  LSGD_CUDA(cudaLaunchKernelEx(&cfg, gemm_tf32x3_kernel<A_MN, B_MN, PAIR, EPI, WS>, p.a_hi, p.a_lo, p.b_hi, p.b_lo,
                                p.K / p.splits, p.splits, p.ep));
 }
 
@@ -880,6 +934,12 @@ void launch_pair_epi(const GemmPlan& p, cudaStream_t st) {
 }
 template <int PAIR>
 void launch_pair(const GemmPlan& p, cudaStream_t st) {
+  if (p.ws) {  // the two weight-reading GEMMs: forward (W K-major) and input gradient (W MN-major)
+    check<Error>(!p.a_mn && ((p.epi == kFwd && !p.b_mn) || (p.epi == kIgrad && p.b_mn)), "gemm: unsupported WS form");
+    if (p.epi == kFwd) launch_variant<false, false, PAIR, kFwd, true>(p, st);
+    else launch_variant<false, true, PAIR, kIgrad, true>(p, st);
+    return;
+  }
   if (p.epi == kFwd) launch_pair_epi<PAIR, kFwd>(p, st);
   else if (p.epi == kWgrad && p.ep.fuse_upd) launch_pair_epi<PAIR, kWgradUpd>(p, st);
   else if (p.epi == kWgrad) launch_pair_epi<PAIR, kWgrad>(p, st);
@@ -915,7 +975,7 @@ int choose_splits(int M, int N, int K, int pair) {
 }
 
 GemmPlan make_plan(const OpView& a_hi, const float* a_lo, const OpView& b_hi, const float* b_lo, int epi,
-                   const EpiParams& ep, float* partial, size_t partial_elems) {
+                   const EpiParams& ep, float* partial, size_t partial_elems, const float* b_raw = nullptr) {
   GemmPlan p;
   p.a_mn = a_hi.mn;
   p.b_mn = b_hi.mn;
@@ -936,6 +996,13 @@ GemmPlan make_plan(const OpView& a_hi, const float* a_lo, const OpView& b_hi, co
   OpView bl = b_hi;
   bl.ptr = b_lo;
   p.b_lo = make_map(bl, BN / p.pair);
+  if (b_raw) {  // split the weights in shared memory: B is read once, as fp32
+    OpView br = b_hi;
+    br.ptr = b_raw;
+    p.b_hi = make_map(br, BN / p.pair);
+    p.b_lo = p.b_hi;
+    p.ws = true;
+  }
   p.epi = epi;
   p.ep = ep;
   const MnGeometry& g = mn_geometry();
@@ -977,7 +1044,17 @@ bool tc_shapes_supported(const std::vector<int32_t>& layers, int batch) {
   return layers.size() >= 2;
 }
 
-void tc_alloc(TcWorkspace& ws, const Layout& L, int batch, int n_features) {
+bool tc_weight_split_in_smem() {
+  static const bool on = [] {
+    const char* e = std::getenv("LSGD_TC_WSPLIT");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
+void tc_alloc(TcWorkspace& ws, const Layout& L, int batch, int n_features, const float* w_master) {
+  const float* w_raw = (w_master && tc_weight_split_in_smem()) ? w_master : nullptr;
+  ws.weights_split_in_smem = w_raw != nullptr;
   static const size_t probe_align = std::getenv("LSGD_TC_ALIGN") ? std::strtoull(std::getenv("LSGD_TC_ALIGN"), nullptr, 10) : 0;
   auto dalloc = [&](size_t elems) {
     void* p = nullptr;
@@ -1027,7 +1104,7 @@ void tc_alloc(TcWorkspace& ws, const Layout& L, int batch, int n_features) {
       ep.out_lo = last ? nullptr : ws.act_lo[static_cast<size_t>(k)];
       ep.relu = last ? 0 : 1;
       tl->fwd = make_plan(OpView{in_hi, B, ni, ni, false}, in_lo, OpView{wk_hi, no, ni, ni, false}, wk_lo, kFwd, ep,
-                          ws.partial, ws.partial_elems);
+                          ws.partial, ws.partial_elems, w_raw ? w_raw + L.w_off[static_cast<size_t>(k)] : nullptr);
     }
     // weight grad: dW_k[no, ni] = delta_k^T[no, B] . in[B, ni] / B  (both operands read MN-major)
     {
@@ -1052,7 +1129,8 @@ void tc_alloc(TcWorkspace& ws, const Layout& L, int batch, int n_features) {
       ep.mask = ws.act[static_cast<size_t>(k - 1)];
       ep.ldm = ni;
       tl->igrad = make_plan(OpView{ws.dlt_hi[di], B, no, no, false}, ws.dlt_lo[di], OpView{wk_hi, ni, no, ni, true},
-                            wk_lo, kIgrad, ep, ws.partial, ws.partial_elems);
+                            wk_lo, kIgrad, ep, ws.partial, ws.partial_elems,
+                            w_raw ? w_raw + L.w_off[static_cast<size_t>(k)] : nullptr);
       tl->has_igrad = true;
     }
     ws.layers.push_back(tl);
@@ -1246,10 +1324,10 @@ void tc_debug_step(const std::vector<int32_t>& layers, int batch, const float* w
   LSGD_CUDA(cudaSetDevice(0));
   Layout L(layers);
   TcWorkspace ws;
-  tc_alloc(ws, L, batch, layers[0]);
   float *w = nullptr, *x = nullptr, *grad = nullptr, *sl = nullptr, *loss = nullptr;
   int32_t* y = nullptr;
   LSGD_CUDA(cudaMalloc(&w, sizeof(float) * L.n_params));
+  tc_alloc(ws, L, batch, layers[0], w);
   LSGD_CUDA(cudaMalloc(&grad, sizeof(float) * L.n_params));
   LSGD_CUDA(cudaMalloc(&x, sizeof(float) * batch * layers[0]));
   LSGD_CUDA(cudaMalloc(&y, sizeof(int32_t) * batch));

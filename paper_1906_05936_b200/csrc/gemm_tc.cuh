@@ -33,11 +33,14 @@ struct TcWorkspace {
   float* partial = nullptr;    // split-K workspace
   size_t partial_elems = 0;
   std::vector<TcLayer*> layers;
+  bool weights_split_in_smem = false;  // the updates need not write w_hi / w_lo
 };
 
 // Every layer width a multiple of 256 and the local batch a multiple of 128 (tile 128 x 256, BK = 32).
 bool tc_shapes_supported(const std::vector<int32_t>& layers, int batch);
-void tc_alloc(TcWorkspace& ws, const Layout& L, int batch, int n_features);
+// w_master (the fp32 weights, fixed address): when given (and LSGD_TC_WSPLIT != 0) the forward and input-gradient
+// GEMMs read it raw and split it in shared memory, so w_hi / w_lo need not be kept current.
+void tc_alloc(TcWorkspace& ws, const Layout& L, int batch, int n_features, const float* w_master = nullptr);
 void tc_free(TcWorkspace& ws);
 // w -> (w_hi, w_lo) for the whole parameter vector (initial parameters; afterwards the fused update writes it).
 void tc_split_weights(TcWorkspace& ws, const Layout& L, const float* w, cudaStream_t st, LaunchCounter& lc);

@@ -564,7 +564,7 @@ class RankImpl final : public Rank {
       LSGD_CUDA(cudaMalloc(&w.idx, sizeof(int32_t) * B_));
       LSGD_CUDA(cudaMalloc(&w.sample_loss, sizeof(T) * B_));
       if (use_tc_) {
-        tc_alloc(w.tc, L_, B_, d);  // owns activations and deltas of the tensor-core path
+        tc_alloc(w.tc, L_, B_, d, reinterpret_cast<const float*>(w.w));  // activations, deltas, plans
       } else {
         for (int k = 0; k < L_.depth(); ++k) {
           T* a = nullptr;
@@ -1103,7 +1103,7 @@ class RankImpl final : public Rank {
     a.loss_out = bk.loss ? w.loss_hist + (u % kLossCap) : nullptr;
     a.bad = bad_dev_;
     static const bool probe_nosplit = std::getenv("LSGD_B200_PROBE_NOSPLIT") != nullptr;  // perf probe: WRONG math
-    if (use_tc_ && !probe_nosplit) {
+    if (use_tc_ && !probe_nosplit && !w.tc.weights_split_in_smem) {
       a.w_hi = w.tc.w_hi + bk.pstart;
       a.w_lo = w.tc.w_lo + bk.pstart;
     }
