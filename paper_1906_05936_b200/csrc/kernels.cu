@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(256) update_kernel(UpdateArgs<T> a) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = i0 + u * stride;
-      if (i < nvec) {
+      if (i < nvec && !(i * V >= a.skip_lo && i * V < a.skip_hi)) {
         const int64_t e = i * V;
         const int64_t j = e / a.slice_len;  // slice_len is a multiple of V: a vector never straddles slices
         d[u] = ld16(a.slices.p[j] + (e - j * a.slice_len));
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(256) update_kernel(UpdateArgs<T> a) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = i0 + u * stride;
-      if (i >= nvec) continue;
+      if (i >= nvec || (i * V >= a.skip_lo && i * V < a.skip_hi)) continue;
       const int64_t e = i * V;
 #pragma unroll
       for (int q = 0; q < V; ++q) {
@@ -347,6 +347,7 @@ __global__ void __launch_bounds__(256) update_kernel(UpdateArgs<T> a) {
   }
   const int64_t end = a.n_params + (a.loss_out ? 1 : 0);
   for (int64_t e = nvec * V + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < end; e += stride) {
+    if (e >= a.skip_lo && e < a.skip_hi) continue;
     const int64_t j = e / a.slice_len;
     T d = pre_delta(a.slices.p[j][e - j * a.slice_len], a);
     if (e == a.n_params) {  // the loss slot rides the same reduction (executors.cpp:59-63, 226)
@@ -493,6 +494,77 @@ __global__ void __launch_bounds__(256) copy_pairs_kernel(const __grid_constant__
     for (int64_t e = nvec * V + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < len; e += stride)
       dp[e] = sp[e];
   }
+}
+
+template <typename T, bool EXACT>
+__device__ __forceinline__ void gu_update_one(const GlobalUpdateArgs<T>& a, int64_t idx, T d, bool& bad) {
+  if (idx < a.n_params) {
+    T w = a.w[idx], v = a.mode ? a.v[idx] : T(0);
+    UpdateArgs<T> u{};
+    u.mode = a.mode;
+    u.lr = a.lr;
+    u.momentum = a.momentum;
+    u.weight_decay = a.weight_decay;
+    sgd_one<T, EXACT>(w, v, d, u);
+    a.w[idx] = w;
+    if (a.mode) a.v[idx] = v;
+    bad |= !isfinite(w);
+  } else if (idx == a.n_params && a.loss_out) {
+    *a.loss_out = d;
+  }
+}
+
+template <typename T, bool EXACT>
+__global__ void __launch_bounds__(256) global_update_kernel(const __grid_constant__ GlobalUpdateArgs<T> a,
+                                                            bool vec_params) {
+  constexpr int V = Vec<T>::kN;
+  const int64_t nvec = a.len / V;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  UpdateArgs<T> u{};
+  u.mode = a.mode;
+  u.lr = a.lr;
+  u.momentum = a.momentum;
+  u.weight_decay = a.weight_decay;
+  bool bad = false;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nvec; i += stride) {
+    const int64_t e = i * V;
+    Vec<T> s = ld16(a.src.p[0] + e);  // this group's slot sum, recomputed (K6 order)
+    for (int m = 1; m < a.k; ++m) {
+      const Vec<T> x = ld16(a.src.p[m] + e);
+#pragma unroll
+      for (int q = 0; q < V; ++q) s.v[q] = Rn<T>::add(s.v[q], x.v[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      if (a.add_zero) s.v[q] = Rn<T>::add(s.v[q], T(0));
+      if (a.divisor != T(0)) s.v[q] = Rn<T>::div(s.v[q], a.divisor);
+    }
+    Vec<T> r = a.g == 0 ? s : ld16(a.gsum.p[0] + e);  // K7: ascending group order
+    for (int gg = 1; gg < a.G; ++gg) {
+      const Vec<T> x = gg == a.g ? s : ld16(a.gsum.p[gg] + e);
+#pragma unroll
+      for (int q = 0; q < V; ++q) r.v[q] = Rn<T>::add(r.v[q], x.v[q]);
+    }
+    for (int d = 0; d < a.n_push; ++d) st16(a.push.p[d] + e, r);  // broadcast to the other members
+    const int64_t i0 = a.first + e;
+    if (vec_params && i0 + V <= a.n_params) {  // K8 on the owner's own parameters
+      Vec<T> w = ld16(a.w + i0), v;
+      if (a.mode) v = ld16(a.v + i0);
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        T vq = a.mode ? v.v[q] : T(0);
+        sgd_one<T, EXACT>(w.v[q], vq, r.v[q], u);
+        if (a.mode) v.v[q] = vq;
+        bad |= !isfinite(w.v[q]);
+      }
+      st16(a.w + i0, w);
+      if (a.mode) st16(a.v + i0, v);
+    } else {
+#pragma unroll
+      for (int q = 0; q < V; ++q) gu_update_one<T, EXACT>(a, i0 + q, r.v[q], bad);
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x % 32) == 0) atomicOr(a.bad, 1u);
 }
 
 __global__ void signal_many_kernel(SignalList fl, int n, unsigned long long v) {
@@ -682,6 +754,23 @@ void launch_copy_pairs(SrcList<T> src, DstList<T> dst, int n_pairs, int64_t len,
   LSGD_CUDA(cudaGetLastError());
 }
 
+template <typename T>
+void launch_global_update(const GlobalUpdateArgs<T>& a, bool exact, cudaStream_t st, LaunchCounter& lc) {
+  bool aligned = a.len % Vec<T>::kN == 0;
+  for (int i = 0; i < a.k; ++i) aligned = aligned && (reinterpret_cast<uintptr_t>(a.src.p[i]) & 15u) == 0;
+  for (int g = 0; g < a.G; ++g)
+    if (g != a.g) aligned = aligned && (reinterpret_cast<uintptr_t>(a.gsum.p[g]) & 15u) == 0;
+  for (int d = 0; d < a.n_push; ++d) aligned = aligned && (reinterpret_cast<uintptr_t>(a.push.p[d]) & 15u) == 0;
+  check<Error>(aligned, "global_update: slices must be 16-byte aligned vectors");
+  const bool vec_params = (reinterpret_cast<uintptr_t>(a.w + a.first) & 15u) == 0 &&
+                          (a.v == nullptr || (reinterpret_cast<uintptr_t>(a.v + a.first) & 15u) == 0);
+  const int g = grid_for(a.len / Vec<T>::kN + 1, 256, 148 * 8);
+  if (exact) global_update_kernel<T, true><<<g, 256, side_smem(), st>>>(a, vec_params);
+  else global_update_kernel<T, false><<<g, 256, side_smem(), st>>>(a, vec_params);
+  ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
+}
+
 void launch_signal_many(SignalList flags, int n, unsigned long long value, cudaStream_t st, LaunchCounter& lc) {
   signal_many_kernel<<<1, 32, 0, st>>>(flags, n, value);
   ++lc.n;
@@ -723,7 +812,8 @@ void launch_to_f64(const T* src, int64_t n, double* dst, cudaStream_t st, Launch
   template void launch_push<T>(const T*, int64_t, DstList<T>, int, cudaStream_t, LaunchCounter&);                 \
   template void launch_reduce_push<T>(SrcList<T>, int, int64_t, DstList<T>, int, bool, T, cudaStream_t,              \
                                       LaunchCounter&);                                                             \
-  template void launch_copy_pairs<T>(SrcList<T>, DstList<T>, int, int64_t, cudaStream_t, LaunchCounter&);
+  template void launch_copy_pairs<T>(SrcList<T>, DstList<T>, int, int64_t, cudaStream_t, LaunchCounter&);         \
+  template void launch_global_update<T>(const GlobalUpdateArgs<T>&, bool, cudaStream_t, LaunchCounter&);
 
 LSGD_INSTANTIATE(float)
 LSGD_INSTANTIATE(double)

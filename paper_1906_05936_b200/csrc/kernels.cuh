@@ -71,6 +71,7 @@ struct UpdateArgs {
   unsigned* bad;      // OR-ed 1 when a non-finite parameter is produced
   float* w_hi;        // fp32 only, may be null
   float* w_lo;
+  int64_t skip_lo = 0, skip_hi = 0;  // bucket-local elements [skip_lo, skip_hi) are updated elsewhere (own slot)
 };
 template <typename T>
 void launch_update(const UpdateArgs<T>& a, bool exact, cudaStream_t st, LaunchCounter& lc);
@@ -83,6 +84,34 @@ struct DstList {
 };
 template <typename T>
 void launch_push(const T* src, int64_t len, DstList<T> dst, int n_dst, cudaStream_t st, LaunchCounter& lc);
+
+// --- K7 + broadcast + K8 for the owner's own slot, fused: per element of slot j the owner recomputes its group's
+// ordered sum (+0.0, /N) from the local member sub-slices, adds the other groups' sums (local gstage) in ascending
+// group order, stores the average into the other members' gfull (NVLink) and applies the SGD / momentum update to its
+// own parameters of that slot (same arithmetic as update_kernel; the loss slot goes to the loss history). The own
+// slot's average never touches HBM.
+template <typename T>
+struct GlobalUpdateArgs {
+  SrcList<T> src;       // k member sub-slices of the slot (local), ascending member order
+  int k = 1;
+  SrcList<T> gsum;      // [G]: other groups' slot sums (local gstage); own entry unused
+  int G = 1, g = 0;
+  bool add_zero = false;
+  T divisor = T(0);
+  int64_t len = 0;      // slot length S
+  DstList<T> push;      // the other members' gfull for this slot
+  int n_push = 0;
+  int64_t first = 0;    // bucket-local index of slot element 0
+  int64_t n_params = 0; // bucket parameters (index n_params = the loss slot, beyond = padding)
+  T* w = nullptr;       // bucket parameter 0
+  T* v = nullptr;
+  int mode = 0;
+  T lr = T(0), momentum = T(0), weight_decay = T(0);
+  T* loss_out = nullptr;
+  unsigned* bad = nullptr;
+};
+template <typename T>
+void launch_global_update(const GlobalUpdateArgs<T>& a, bool exact, cudaStream_t st, LaunchCounter& lc);
 
 // --- push exchange (K6/K7 without remote reads): ordered sum of local sources written to n destinations (local or
 // peer), and member -> owner scatter copies (pair p: src_p[0, len) -> dst_p). Grids capped at LSGD_B200_COMM_CTAS.

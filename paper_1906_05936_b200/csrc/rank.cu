@@ -142,6 +142,7 @@ class RankImpl final : public Rank {
     else upd_ = main_;
     for (int b = 0; b < kMaxBuckets; ++b) LSGD_CUDA(cudaEventCreateWithFlags(&ev_upd_[b], cudaEventDisableTiming));
     for (int b = 0; b < kMaxBuckets; ++b) LSGD_CUDA(cudaEventCreateWithFlags(&ev_dx_[b], cudaEventDisableTiming));
+    for (int b = 0; b < kMaxBuckets; ++b) LSGD_CUDA(cudaEventCreateWithFlags(&ev_gupd_[b], cudaEventDisableTiming));
     for (int b = 0; b < kMaxBuckets; ++b) LSGD_CUDA(cudaEventCreateWithFlags(&ev_bucket_[b], cudaEventDisableTiming));
     LSGD_CUDA(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming));
     void* to = nullptr;
@@ -211,6 +212,7 @@ class RankImpl final : public Rank {
     }
     for (int b = 0; b < kMaxBuckets; ++b) cudaEventDestroy(ev_upd_[b]);
     for (int b = 0; b < kMaxBuckets; ++b) cudaEventDestroy(ev_dx_[b]);
+    for (int b = 0; b < kMaxBuckets; ++b) cudaEventDestroy(ev_gupd_[b]);
     cudaEventDestroy(join_ev_);
     if (base_ev_) cudaEventDestroy(base_ev_);
     if (io_) {
@@ -791,6 +793,13 @@ class RankImpl final : public Rank {
     const bool exchange = !flat_nccl() && !reduce_folded() && alg_ != LSGD_B200_SEQUENTIAL;
     return exchange && split_ && use_tc_ && k_ > 1;
   }
+  // Push exchange (one worker per GPU, ordered global sum): the owner's K7 + broadcast + K8 for its own slot run as
+  // one kernel on the comm stream; apply_bucket then updates the other members' slots only.
+  bool own_slot_fused() const {
+    const bool exchange = !flat_nccl() && !reduce_folded() && alg_ != LSGD_B200_SEQUENTIAL;
+    return exchange && split_ && slice_comm_ == nullptr;
+  }
+
   // One worker, one group (N = 1): the gradient is final when produced, so the update runs in the producers'
   // epilogues (dW GEMM, bias) and the separate update pass over g disappears.
   bool fused_update() const {
@@ -1025,28 +1034,61 @@ class RankImpl final : public Rank {
       arrived.f[m] = peer_arrived(members[static_cast<size_t>(m)], b, me);
     }
     const bool lsgd = alg_ == LSGD_B200_LSGD;
+    if (own_slot_fused()) {
+      // G > 1: the slot sum goes to the other groups' slot owners only (this owner recomputes it below)
+      if (G_ > 1) {
+        DstList<T> gdst{};
+        SignalList gsig{};
+        int n = 0;
+        for (int g = 0; g < G_; ++g) {
+          if (g == w.g) continue;
+          const int owner = g * k_ + me;
+          gdst.p[n] = peer_gstage(owner, par, w.g) + bk.goff;
+          gsig.f[n++] = peer_flag_word(owner, kGsum + b * kMaxPeers + w.g);
+        }
+        {
+          Timed tm(this, "reduce", st);
+          launch_reduce_push<T>(src, k_, bk.S, gdst, n, lsgd, static_cast<T>(N_), st, lc_);
+        }
+        launch_signal_many(gsig, n, round, st, lc_);
+        wait_own(w, kGsum + b * kMaxPeers, G_, w.g, round, st);
+      }
+      // K7 + broadcast to the other members + K8 of this owner's slot in one pass
+      GlobalUpdateArgs<T> ga;
+      ga.src = src;
+      ga.k = k_;
+      for (int g = 0; g < G_; ++g) ga.gsum.p[g] = w.blk_gstage(par, g) + bk.goff;
+      ga.G = G_;
+      ga.g = w.g;
+      ga.add_zero = lsgd;
+      ga.divisor = static_cast<T>(N_);
+      ga.len = bk.S;
+      SignalList others{};
+      for (int m = 0; m < k_; ++m) {
+        if (m == me) continue;
+        others.f[ga.n_push] = peer_arrived(members[static_cast<size_t>(m)], b, me);
+        ga.push.p[ga.n_push++] = peer_gfull(members[static_cast<size_t>(m)]) + bk.poff + static_cast<int64_t>(me) * bk.S;
+      }
+      ga.first = static_cast<int64_t>(me) * bk.S;
+      ga.n_params = bk.n;
+      ga.w = w.w + bk.pstart;
+      ga.v = w.v ? w.v + bk.pstart : nullptr;
+      ga.mode = spec_.c.mode;
+      ga.lr = static_cast<T>(spec_.lr(t));
+      ga.momentum = static_cast<T>(spec_.c.momentum);
+      ga.weight_decay = static_cast<T>(spec_.c.weight_decay);
+      ga.loss_out = bk.loss ? w.loss_hist + (t % kLossCap) : nullptr;
+      ga.bad = bad_dev_;
+      {
+        Timed tm(this, "global", st);
+        launch_global_update<T>(ga, exact_, st, lc_);
+      }
+      if (ga.n_push) launch_signal_many(others, ga.n_push, round, st, lc_);
+      LSGD_CUDA(cudaEventRecord(ev_gupd_[b], st));
+      return;
+    }
     if (G_ == 1) {
       Timed tm(this, "reduce", st);
-      launch_reduce_push<T>(src, k_, bk.S, gfull, k_, lsgd, static_cast<T>(N_), st, lc_);
-    } else if (slice_comm_ == nullptr) {
-      DstList<T> gdst{};
-      SignalList gsig{};
-      int n = 0;
-      for (int g = 0; g < G_; ++g) {
-        const int owner = g * k_ + me;
-        gdst.p[g] = peer_gstage(owner, par, w.g) + bk.goff;
-        if (g != w.g) gsig.f[n++] = peer_flag_word(owner, kGsum + b * kMaxPeers + w.g);
-      }
-      {
-        Timed tm(this, "reduce", st);
-        launch_reduce_push<T>(src, k_, bk.S, gdst, G_, lsgd, static_cast<T>(N_), st, lc_);
-      }
-      launch_signal_many(gsig, n, round, st, lc_);
-      wait_own(w, kGsum + b * kMaxPeers, G_, w.g, round, st);
-      SrcList<T> gsrc{};
-      for (int g = 0; g < G_; ++g) gsrc.p[g] = w.blk_gstage(par, g) + bk.goff;
-      Timed tm(this, "global", st);
-      launch_reduce_push<T>(gsrc, G_, bk.S, gfull, k_, false, T(0), st, lc_);
     } else {
       DstList<T> sdst{};
       sdst.p[0] = w.s[par] + bk.goff;
@@ -1084,11 +1126,25 @@ class RankImpl final : public Rank {
       }
       if (flat_nccl()) a.post_div = static_cast<T>(N_);  // the per-worker /N after the flat allreduce (:170)
     } else {
-      FlagList fl{};  // the k sub-slices of round u have been pushed into this worker's gfull
-      for (int j = 0; j < k_; ++j) fl.f[j] = peer_arrived(w.id, b, j);
-      launch_wait_flags(fl, k_, static_cast<unsigned long long>(u + 1), timeout_ns(), timed_out_dev_, st, lc_);
+      const bool own = own_slot_fused();  // this worker's own slot was updated by its fused global kernel
+      FlagList fl{};  // the other sub-slices of round u have been pushed into this worker's gfull
+      int nf = 0;
+      for (int j = 0; j < k_; ++j)
+        if (!own || j != w.j) fl.f[nf++] = peer_arrived(w.id, b, j);
+      if (nf) launch_wait_flags(fl, nf, static_cast<unsigned long long>(u + 1), timeout_ns(), timed_out_dev_, st, lc_);
       a.slices.p[0] = w.gfull + bk.poff;
       a.slice_len = bk.S * k_;
+      if (own) {
+        a.skip_lo = static_cast<int64_t>(w.j) * bk.S;
+        a.skip_hi = a.skip_lo + bk.S;
+        if (k_ == 1) {  // nothing left to update here
+          if (b == 0) {
+            phase_mark(wi, u, 4, 1, st);
+            phase_mark(wi, u, 5, 0, st);
+          }
+          return;
+        }
+      }
     }
     if (b == 0) {
       phase_mark(wi, u, 4, 1, st);
@@ -1246,6 +1302,7 @@ class RankImpl final : public Rank {
         for (int b : LB[static_cast<size_t>(k)]) {
           if (reduce_folded()) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_bucket_[b], 0));
           apply_bucket(w, b, t, upd_);
+          if (own_slot_fused()) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_gupd_[b], 0));  // own slot (comm stream)
           LSGD_CUDA(cudaEventRecord(ev_upd_[b], upd_));
         }
       }
@@ -1256,7 +1313,10 @@ class RankImpl final : public Rank {
     if (alg_ != LSGD_B200_LSGD) {  // sequential / csgd: synchronous update in the same block (executors.cpp:172-177)
       current_phase() = "update";
       for (auto& w : ws_) {
-        for (int b = 0; b < NB; ++b) apply_bucket(w, b, t, main_);
+        for (int b = 0; b < NB; ++b) {
+          apply_bucket(w, b, t, main_);
+          if (own_slot_fused()) LSGD_CUDA(cudaStreamWaitEvent(main_, ev_gupd_[b], 0));
+        }
         after_update(w, t, main_);
       }
       ++applied_;
@@ -1289,6 +1349,7 @@ class RankImpl final : public Rank {
   cudaStream_t main_ = nullptr, comm_ = nullptr, comm2_ = nullptr;
   cudaEvent_t ev_bucket_[kMaxBuckets] = {};
   cudaEvent_t ev_upd_[kMaxBuckets] = {};
+  cudaEvent_t ev_gupd_[kMaxBuckets] = {};  // per bucket: the owner's fused global + update issued (comm stream)
   cudaEvent_t ev_dx_[kMaxBuckets] = {};
   cudaEvent_t base_ev_ = nullptr;  // timeline origin (set_timing)
   cudaEvent_t join_ev_ = nullptr;
