@@ -144,3 +144,25 @@ def test_single_worker_fused_update_is_bitwise_the_update_pass(mode):
     ref = Oracle("port").run_train(spec, history=True)["history"]
     dev = np.linalg.norm(fused - ref, axis=1) / np.linalg.norm(ref, axis=1)
     assert dev.max() <= 1e-5, dev.max()
+
+
+def test_weight_split_in_shared_memory_is_bitwise_the_hbm_split():
+    """The forward / dX GEMMs split the fp32 weights into TF32 hi/lo in shared memory (default) — the same values the
+    separate split pass wrote to HBM (LSGD_TC_WSPLIT=0 path), so the iterates are bitwise identical."""
+    cfg = tc_cfg(mode="momentum", n_workers=1, iterations=6)
+    cfg.b200.gemm = "tcgen05"
+    ws = lsgd.run_train(cfg).param_history
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_1906_05936_b200 as lsgd\n"
+        "c = lsgd.TrainConfig(algorithm='lsgd', n_workers=1, n_groups=1, layer_sizes=[256, 512, 256],\n"
+        "    n_samples=2048, n_features=256, n_classes=256, spread=10.0, local_batch=128, iterations=6,\n"
+        "    mode='momentum', record_history=True)\n"
+        "c.b200.n_devices = 1; c.b200.gemm = 'tcgen05'\n"
+        "np.save(sys.argv[1], lsgd.run_train(c).param_history)\n" % ROOT)
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "h.npy")
+        env = dict(os.environ, LSGD_TC_WSPLIT="0")
+        subprocess.run([sys.executable, "-c", code, out], check=True, env=env, cwd=ROOT)
+        hbm = np.load(out)
+    assert np.array_equal(ws.view(np.uint64), hbm.view(np.uint64))
