@@ -36,7 +36,9 @@ constexpr int STAGE_RING_BYTES = 192 * 1024;
 constexpr int EPI_STAGE_BYTES = 32 * 32 * 4;  // per epilogue warp: one 32 x 32 fp32 chunk (4 KB)
 // fused update: per epilogue warp, w and v of one 32 x 32 chunk (8 KB), double-buffered (cp.async one chunk ahead)
 constexpr int UPD_PREF_BYTES = 2 * 2 * EPI_STAGE_BYTES;
-enum : int { kFwd = 0, kWgrad = 1, kIgrad = 2, kRaw = 3, kWgradUpd = 4 };  // kWgradUpd: dW + fused update
+// kWgradUpd: dW + fused update; kWgradScat: dW scattered to the sub-slice owners (each its own instantiation, so the
+// plain weight-gradient kernel carries neither path)
+enum : int { kFwd = 0, kWgrad = 1, kIgrad = 2, kRaw = 3, kWgradUpd = 4, kWgradScat = 5 };
 template <int PAIR, int EPI = kFwd, bool WS = false>
 struct Cfg {
   static constexpr int B_ROWS = BN / PAIR;                          // B rows staged by one CTA
@@ -297,7 +299,7 @@ __device__ __forceinline__ void epi_vec4(const EpiParams& ep, int row, int col, 
       o[i] = __fadd_rn(o[i], b[i]);
       if (ep.relu && o[i] < 0.f) o[i] = 0.f;
     }
-  } else if (epi == kWgrad || epi == kWgradUpd) {
+  } else if (epi == kWgrad || epi == kWgradUpd || epi == kWgradScat) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) o[i] = ep.div_pow2 ? o[i] * ep.div_inv : __fdiv_rn(o[i], ep.div);  // x*2^-k == x/2^k
   } else {
@@ -311,7 +313,7 @@ __device__ __forceinline__ void epi_vec4(const EpiParams& ep, int row, int col, 
     if (fused_update4(ep.upd, at, o, upd_w4(ep.upd, at), upd_v4(ep.upd, at))) atomicOr(ep.upd.bad, 1u);
     return;
   }
-  float* outp = (epi == kWgrad && ep.scat.n) ? scatter_at(scat_table, ep.scat.e0 + at) : ep.out + at;
+  float* outp = epi == kWgradScat ? scatter_at(scat_table, ep.scat.e0 + at) : ep.out + at;
   *reinterpret_cast<float4*>(outp) = make_float4(o[0], o[1], o[2], o[3]);
   if (ep.out_hi) {
     const float h0 = tf32_rna(o[0]), h1 = tf32_rna(o[1]), h2 = tf32_rna(o[2]), h3 = tf32_rna(o[3]);
@@ -942,6 +944,7 @@ void launch_pair(const GemmPlan& p, cudaStream_t st) {
   }
   if (p.epi == kFwd) launch_pair_epi<PAIR, kFwd>(p, st);
   else if (p.epi == kWgrad && p.ep.fuse_upd) launch_pair_epi<PAIR, kWgradUpd>(p, st);
+  else if (p.epi == kWgrad && p.ep.scat.n) launch_pair_epi<PAIR, kWgradScat>(p, st);
   else if (p.epi == kWgrad) launch_pair_epi<PAIR, kWgrad>(p, st);
   else launch_pair_epi<PAIR, kIgrad>(p, st);
 }
@@ -958,6 +961,7 @@ void run_plan(const GemmPlan& p, cudaStream_t st, LaunchCounter& lc) {
     int grid = static_cast<int>(std::min<int64_t>((work + 255) / 256, 148 * 8));
     if (p.epi == kFwd) splitk_reduce_kernel<kFwd><<<grid, 256, 0, st>>>(p.splits, p.ep);
     else if (p.epi == kWgrad && p.ep.fuse_upd) splitk_reduce_kernel<kWgradUpd><<<grid, 256, 0, st>>>(p.splits, p.ep);
+    else if (p.epi == kWgrad && p.ep.scat.n) splitk_reduce_kernel<kWgradScat><<<grid, 256, 0, st>>>(p.splits, p.ep);
     else if (p.epi == kWgrad) splitk_reduce_kernel<kWgrad><<<grid, 256, 0, st>>>(p.splits, p.ep);
     else splitk_reduce_kernel<kIgrad><<<grid, 256, 0, st>>>(p.splits, p.ep);
     ++lc.n;
