@@ -539,13 +539,25 @@ __global__ void __launch_bounds__(256) global_update_kernel(const __grid_constan
       if (a.add_zero) s.v[q] = Rn<T>::add(s.v[q], T(0));
       if (a.divisor != T(0)) s.v[q] = Rn<T>::div(s.v[q], a.divisor);
     }
-    Vec<T> r = a.g == 0 ? s : ld16(a.gsum.p[0] + e);  // K7: ascending group order
+    auto group_sum = [&](int gg) {  // the other groups' K6 results (recomputed from raw payloads when k = 1)
+      Vec<T> x = ld16(a.gsum.p[gg] + e);
+      if (a.gsum_raw) {
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          if (a.add_zero) x.v[q] = Rn<T>::add(x.v[q], T(0));
+          if (a.divisor != T(0)) x.v[q] = Rn<T>::div(x.v[q], a.divisor);
+        }
+      }
+      return x;
+    };
+    Vec<T> r = a.g == 0 ? s : group_sum(0);  // K7: ascending group order
     for (int gg = 1; gg < a.G; ++gg) {
-      const Vec<T> x = gg == a.g ? s : ld16(a.gsum.p[gg] + e);
+      const Vec<T> x = gg == a.g ? s : group_sum(gg);
 #pragma unroll
       for (int q = 0; q < V; ++q) r.v[q] = Rn<T>::add(r.v[q], x.v[q]);
     }
     for (int d = 0; d < a.n_push; ++d) st16(a.push.p[d] + e, r);  // broadcast to the other members
+    if (a.out_local) st16(a.out_local + e, r);
     const int64_t i0 = a.first + e;
     if (vec_params && i0 + V <= a.n_params) {  // K8 on the owner's own parameters
       Vec<T> w = ld16(a.w + i0), v;
@@ -761,6 +773,7 @@ void launch_global_update(const GlobalUpdateArgs<T>& a, bool exact, cudaStream_t
   for (int g = 0; g < a.G; ++g)
     if (g != a.g) aligned = aligned && (reinterpret_cast<uintptr_t>(a.gsum.p[g]) & 15u) == 0;
   for (int d = 0; d < a.n_push; ++d) aligned = aligned && (reinterpret_cast<uintptr_t>(a.push.p[d]) & 15u) == 0;
+  if (a.out_local) aligned = aligned && (reinterpret_cast<uintptr_t>(a.out_local) & 15u) == 0;
   check<Error>(aligned, "global_update: slices must be 16-byte aligned vectors");
   const bool vec_params = (reinterpret_cast<uintptr_t>(a.w + a.first) & 15u) == 0 &&
                           (a.v == nullptr || (reinterpret_cast<uintptr_t>(a.v + a.first) & 15u) == 0);

@@ -96,11 +96,13 @@ struct GlobalUpdateArgs {
   int k = 1;
   SrcList<T> gsum;      // [G]: other groups' slot sums (local gstage); own entry unused
   int G = 1, g = 0;
+  bool gsum_raw = false; // k = 1: gstage holds the other owners' raw payload (DMA copy), apply (+0.0, /N) here
   bool add_zero = false;
   T divisor = T(0);
   int64_t len = 0;      // slot length S
   DstList<T> push;      // the other members' gfull for this slot
   int n_push = 0;
+  T* out_local = nullptr;  // also store the average here (the copy engines forward it when pushing by DMA)
   int64_t first = 0;    // bucket-local index of slot element 0
   int64_t n_params = 0; // bucket parameters (index n_params = the loss slot, beyond = padding)
   T* w = nullptr;       // bucket parameter 0

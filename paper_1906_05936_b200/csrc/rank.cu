@@ -791,10 +791,20 @@ class RankImpl final : public Rank {
   // The push exchange's scatter is fused into the producers (dW epilogue, bias, loss) on the tensor-core path.
   bool fused_scatter() const {
     const bool exchange = !flat_nccl() && !reduce_folded() && alg_ != LSGD_B200_SEQUENTIAL;
-    return exchange && split_ && use_tc_ && k_ > 1;
+    return exchange && split_ && use_tc_ && k_ > 1 && !dma(2);
   }
   // Push exchange (one worker per GPU, ordered global sum): the owner's K7 + broadcast + K8 for its own slot run as
   // one kernel on the comm stream; apply_bucket then updates the other members' slots only.
+  // Which NVLink transfers go through the copy engines (no SM time, so the dW GEMMs they overlap keep their SMs)
+  // instead of SM stores. LSGD_B200_DMA bit mask: 1 the k = 1 group payload (moves unchanged), 2 the member ->
+  // owner scatter of the dW sub-slices (instead of the fused epilogue stores), 4 the group-sum push, 8 the average
+  // fan-out. Default 1|2 (measured: N=2 +11%, N=4 +2%; 4 and 8 add a local round trip and were slower).
+  int dma_bits() const {
+    static const int v = std::getenv("LSGD_B200_DMA") ? std::atoi(std::getenv("LSGD_B200_DMA")) : 3;
+    return v;
+  }
+  bool dma_push() const { return dma_bits() != 0; }
+  bool dma(int bit) const { return (dma_bits() & bit) != 0; }
   bool own_slot_fused() const {
     const bool exchange = !flat_nccl() && !reduce_folded() && alg_ != LSGD_B200_SEQUENTIAL;
     return exchange && split_ && slice_comm_ == nullptr;
@@ -1019,7 +1029,12 @@ class RankImpl final : public Rank {
       }
       {
         Timed tm(this, "scatter", st);
-        launch_copy_pairs<T>(src, dst, n, bk.S, st, lc_);
+        if (dma(2)) {
+          for (int q = 0; q < n; ++q)
+            LSGD_CUDA(cudaMemcpyAsync(dst.p[q], src.p[q], sizeof(T) * bk.S, cudaMemcpyDeviceToDevice, st));
+        } else {
+          launch_copy_pairs<T>(src, dst, n, bk.S, st, lc_);
+        }
       }
       launch_signal_many(sl, n, round, st, lc_);
       wait_own(w, kStaged + b * kMaxPeers, k_, me, round, st);
@@ -1046,7 +1061,20 @@ class RankImpl final : public Rank {
           gdst.p[n] = peer_gstage(owner, par, w.g) + bk.goff;
           gsig.f[n++] = peer_flag_word(owner, kGsum + b * kMaxPeers + w.g);
         }
-        {
+        if (k_ == 1 && dma(1)) {
+          // one member per group: the group "sum" is the payload itself, so the copy engines move it (no SM time);
+          // the receiving owner applies the group's (+0.0, /N) when it reads it
+          Timed tm(this, "reduce", st);
+          for (int q = 0; q < n; ++q)
+            LSGD_CUDA(cudaMemcpyAsync(gdst.p[q], src.p[0], sizeof(T) * bk.S, cudaMemcpyDeviceToDevice, st));
+        } else if (k_ > 1 && dma(4)) {  // the group sum lands locally, the copy engines forward it
+          Timed tm(this, "reduce", st);
+          DstList<T> loc{};
+          loc.p[0] = w.s[par] + bk.goff;
+          launch_reduce_push<T>(src, k_, bk.S, loc, 1, lsgd, static_cast<T>(N_), st, lc_);
+          for (int q = 0; q < n; ++q)
+            LSGD_CUDA(cudaMemcpyAsync(gdst.p[q], loc.p[0], sizeof(T) * bk.S, cudaMemcpyDeviceToDevice, st));
+        } else {
           Timed tm(this, "reduce", st);
           launch_reduce_push<T>(src, k_, bk.S, gdst, n, lsgd, static_cast<T>(N_), st, lc_);
         }
@@ -1060,6 +1088,7 @@ class RankImpl final : public Rank {
       for (int g = 0; g < G_; ++g) ga.gsum.p[g] = w.blk_gstage(par, g) + bk.goff;
       ga.G = G_;
       ga.g = w.g;
+      ga.gsum_raw = G_ > 1 && k_ == 1 && dma(1);
       ga.add_zero = lsgd;
       ga.divisor = static_cast<T>(N_);
       ga.len = bk.S;
@@ -1079,11 +1108,21 @@ class RankImpl final : public Rank {
       ga.weight_decay = static_cast<T>(spec_.c.weight_decay);
       ga.loss_out = bk.loss ? w.loss_hist + (t % kLossCap) : nullptr;
       ga.bad = bad_dev_;
+      DstList<T> remote = ga.push;
+      const int n_remote = ga.n_push;
+      const bool fan_dma = dma(8) && n_remote > 0;
+      if (fan_dma) {  // average stored locally once, the copy engines fan it out
+        ga.n_push = 0;
+        ga.out_local = w.gbar + bk.goff;
+      }
       {
         Timed tm(this, "global", st);
         launch_global_update<T>(ga, exact_, st, lc_);
       }
-      if (ga.n_push) launch_signal_many(others, ga.n_push, round, st, lc_);
+      if (fan_dma)
+        for (int q = 0; q < n_remote; ++q)
+          LSGD_CUDA(cudaMemcpyAsync(remote.p[q], ga.out_local, sizeof(T) * bk.S, cudaMemcpyDeviceToDevice, st));
+      if (n_remote) launch_signal_many(others, n_remote, round, st, lc_);
       LSGD_CUDA(cudaEventRecord(ev_gupd_[b], st));
       return;
     }
