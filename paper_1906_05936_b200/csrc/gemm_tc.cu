@@ -811,19 +811,12 @@ EncodeFn encode_fn() {
 }
 
 // MN-major operand geometry: TMA swizzle SWIZZLE_128B_ATOM_32B + UMMA layout SWIZZLE_128B_BASE32B, LBO = MN chunk
-// stride, SBO = 4-row K atom stride. LSGD_TC_MN="lbo,sbo,layout,tma_swizzle" overrides it (bring-up only).
+// stride, SBO = 4-row K atom stride.
 struct MnGeometry {
   uint32_t lbo = MN_CHUNK_BYTES, sbo = 512, layout = 1, tma_swizzle = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
 };
 const MnGeometry& mn_geometry() {
-  static MnGeometry g = [] {
-    MnGeometry m;
-    if (const char* s = std::getenv("LSGD_TC_MN")) {
-      unsigned a, b, c, d;
-      if (std::sscanf(s, "%u,%u,%u,%u", &a, &b, &c, &d) == 4) m = MnGeometry{a, b, c, d};
-    }
-    return m;
-  }();
+  static const MnGeometry g;
   return g;
 }
 
@@ -954,8 +947,6 @@ void run_plan(const GemmPlan& p, cudaStream_t st, LaunchCounter& lc) {
   else launch_pair<1>(p, st);
   ++lc.n;
   LSGD_CUDA(cudaGetLastError());
-  static const bool probe_sync = std::getenv("LSGD_TC_SYNC") != nullptr;
-  if (probe_sync) LSGD_CUDA(cudaStreamSynchronize(st));
   if (p.splits > 1) {
     int64_t work = static_cast<int64_t>(p.M) * p.N / 4;
     int grid = static_cast<int>(std::min<int64_t>((work + 255) / 256, 148 * 8));
@@ -1013,8 +1004,7 @@ GemmPlan make_plan(const OpView& a_hi, const float* a_lo, const OpView& b_hi, co
   p.ep.mn_lbo = g.lbo;
   p.ep.mn_sbo = g.sbo;
   p.ep.mn_layout = g.layout;
-  static const bool no_prefetch = std::getenv("LSGD_TC_NOPREFETCH") != nullptr;  // bring-up probe only
-  p.ep.prefetch = no_prefetch ? 0u : 1u;
+  p.ep.prefetch = 1u;
   static const uint32_t probe = std::getenv("LSGD_TC_PROBE") ? std::atoi(std::getenv("LSGD_TC_PROBE")) : 0;
   p.ep.probe = probe;
   int ex = 0;
@@ -1059,15 +1049,11 @@ bool tc_weight_split_in_smem() {
 void tc_alloc(TcWorkspace& ws, const Layout& L, int batch, int n_features, const float* w_master) {
   const float* w_raw = (w_master && tc_weight_split_in_smem()) ? w_master : nullptr;
   ws.weights_split_in_smem = w_raw != nullptr;
-  static const size_t probe_align = std::getenv("LSGD_TC_ALIGN") ? std::strtoull(std::getenv("LSGD_TC_ALIGN"), nullptr, 10) : 0;
   auto dalloc = [&](size_t elems) {
     void* p = nullptr;
-    LSGD_CUDA(cudaMalloc(&p, elems * sizeof(float) + probe_align));
+    LSGD_CUDA(cudaMalloc(&p, elems * sizeof(float)));
     ws.bufs.push_back(p);
-    uintptr_t a = reinterpret_cast<uintptr_t>(p);
-    if (probe_align) a = (a + probe_align - 1) / probe_align * probe_align;
-    if (std::getenv("LSGD_TC_DEBUG")) std::fprintf(stderr, "tc buf %zu elems at %#lx\n", elems, (unsigned long)a);
-    return reinterpret_cast<float*>(a);
+    return static_cast<float*>(p);
   };
   const int B = batch;
   ws.batch = B;
@@ -1143,9 +1129,7 @@ void tc_alloc(TcWorkspace& ws, const Layout& L, int batch, int n_features, const
 }
 
 void tc_free(TcWorkspace& ws) {
-  static const bool leak = std::getenv("LSGD_TC_NOFREE") != nullptr;  // bring-up probe only
-  if (!leak)
-    for (void* p : ws.bufs) cudaFree(p);
+  for (void* p : ws.bufs) cudaFree(p);
   ws.bufs.clear();
   for (TcLayer* l : ws.layers) delete l;
   ws.layers.clear();

@@ -1197,8 +1197,7 @@ class RankImpl final : public Rank {
     a.weight_decay = static_cast<T>(spec_.c.weight_decay);
     a.loss_out = bk.loss ? w.loss_hist + (u % kLossCap) : nullptr;
     a.bad = bad_dev_;
-    static const bool probe_nosplit = std::getenv("LSGD_B200_PROBE_NOSPLIT") != nullptr;  // perf probe: WRONG math
-    if (use_tc_ && !probe_nosplit && !w.tc.weights_split_in_smem) {
+    if (use_tc_ && !w.tc.weights_split_in_smem) {
       a.w_hi = w.tc.w_hi + bk.pstart;
       a.w_lo = w.tc.w_lo + bk.pstart;
     }
