@@ -1281,7 +1281,10 @@ void tc_test_gemm(int a_mn, int b_mn, int epi, int M, int N, int K, int reps, co
   ep.relu = relu;
   ep.div = div;
   OpView va{ah, M, K, a_mn ? M : K, a_mn != 0}, vb{bh, N, K, b_mn ? N : K, b_mn != 0};
-  GemmPlan p = make_plan(va, al, vb, bl, epi, ep, part, pe);
+  // LSGD_TC_TEST_WS=1: the weight-reading forms (forward K-major B, input-gradient MN-major B) split B in SMEM
+  static const bool test_ws = std::getenv("LSGD_TC_TEST_WS") && std::atoi(std::getenv("LSGD_TC_TEST_WS")) != 0;
+  const bool ws_form = !a_mn && ((epi == kFwd && !b_mn) || (epi == kIgrad && b_mn));
+  GemmPlan p = make_plan(va, al, vb, bl, epi, ep, part, pe, test_ws && ws_form ? b : nullptr);
   run_plan(p, 0, lc);
   if (reps > 1 && avg_ms) {  // device-timed repetitions (bring-up / tuning)
     cudaEvent_t e0, e1;
