@@ -63,6 +63,10 @@ struct Bucket {
   int64_t S = 0;       // sub-slice length, multiple of 64 elements
   int64_t poff = 0;    // payload offset (elements, 64-aligned)
   int64_t goff = 0;    // offset inside each slot's s/gbar region (64-aligned)
+  // The weight-gradient GEMM runs per block of consecutive buckets (one launch, contiguous payload): the block's
+  // first bucket carries its row count (0 on the others) and whether it ends with the layer's bias.
+  int blk_rows = 0;
+  bool blk_bias = false;
 };
 
 struct Geometry {

@@ -49,34 +49,49 @@ Geometry::Geometry(const RunSpec& spec, int es) : esize(es) {
     Layout L(spec.layers);
     P = L.n_params;
     check<ConfigError>(L.depth() <= kMaxBuckets, "at most ", kMaxBuckets, " layers are supported");
-    // Row blocks of ~64 MB (fp32) per bucket, block heights a multiple of the 128-row GEMM tile.
-    // LSGD_B200_BUCKET_ELEMS overrides the target (tests force multi-block buckets on small models).
+    // Exchange buckets are row blocks of W_k (heights a multiple of the 128-row GEMM tile): ~16M parameters with
+    // one worker per group, 64M for groups of k >= 2, whose exchange costs a scatter + reduce + global chain and
+    // flag round trips per bucket (2x2: 981k samples/s at 64M vs 925k at 16M, 927k with 16M buckets inside 64M GEMM
+    // blocks). The weight-gradient GEMM runs over blocks of consecutive buckets (LSGD_B200_GEMM_ELEMS; default: one
+    // bucket per block). LSGD_B200_BUCKET_ELEMS overrides the bucket target (tests force multi-bucket layers).
+    const int kk = spec.k();
     const char* env = std::getenv("LSGD_B200_BUCKET_ELEMS");
-    // Default: 16M parameters per bucket; groups of k >= 2 GPUs (whose exchange costs scatter + reduce + global
-    // kernels and flag round trips per bucket) use 64M — measured on 2x2: 988k vs 925k samples/s.
-    const double kDefaultElems = (spec.k() >= 2 ? 64.0 : 16.0) * 1024 * 1024;
-    const double kBucketElems = env ? std::max(1.0, std::atof(env)) : kDefaultElems;
+    const char* genv = std::getenv("LSGD_B200_GEMM_ELEMS");
+    const double kBucketElems = env ? std::max(1.0, std::atof(env)) : (kk >= 2 ? 64.0 : 16.0) * 1024 * 1024;
+    const double kGemmElems = genv ? std::max(kBucketElems, std::atof(genv)) : kBucketElems;
     layer_buckets.resize(static_cast<size_t>(L.depth()));
     // Layer 0's gradient is the last one the backward produces: its exchange + update are the step's exposed tail,
     // so with an exchange (N > 1) it is cut into blocks of half the size.
-    const double kTailElems = spec.N() > 1 ? kBucketElems / 2 : kBucketElems;
+    const bool tail_half = spec.N() > 1;
+    auto split_rows = [](int out, double elems, int in) {  // divisor of out, rows a multiple of the tile quantum
+      int nc = std::max(1, static_cast<int>(std::ceil(static_cast<double>(in) * out / elems)));
+      const int quantum = out % 128 == 0 ? 128 : (out % 8 == 0 ? 8 : out);
+      while (nc > 1 && (out % nc != 0 || (out / nc) % quantum != 0)) --nc;
+      return nc;
+    };
     for (int k = 0; k < L.depth(); ++k) {
       const int in = L.in(k), out = L.out(k);
-      const double target = k == 0 ? kTailElems : kBucketElems;
-      int nc = std::max(1, static_cast<int>(std::ceil(static_cast<double>(in) * out / target)));
-      const int quantum = out % 128 == 0 ? 128 : (out % 8 == 0 ? 8 : out);  // GEMM tile rows
-      while (nc > 1 && (out % nc != 0 || (out / nc) % quantum != 0)) --nc;
-      const int rows = out / nc;
-      for (int c = 0; c < nc; ++c) {
-        Bucket b;
-        b.layer = k;
-        b.row0 = c * rows;
-        b.rows = rows;
-        b.bias = c + 1 == nc;
-        b.pstart = L.w_off[static_cast<size_t>(k)] + static_cast<int64_t>(b.row0) * in;
-        b.n = static_cast<int64_t>(rows) * in + (b.bias ? out : 0);
-        layer_buckets[static_cast<size_t>(k)].push_back(static_cast<int>(buckets.size()));
-        buckets.push_back(b);
+      const double btarget = (k == 0 && tail_half) ? kBucketElems / 2 : kBucketElems;
+      const double gtarget = (k == 0 && tail_half) ? kGemmElems / 2 : kGemmElems;
+      const int ng = split_rows(out, gtarget, in), grows = out / ng;
+      for (int g = 0; g < ng; ++g) {
+        int ne = split_rows(grows, btarget, in);
+        // buckets inside a block must tile the block's contiguous output exactly (no slot padding between them)
+        if ((static_cast<int64_t>(grows / ne) * in) % (64 * kk) != 0) ne = 1;
+        const int rows = grows / ne;
+        for (int c = 0; c < ne; ++c) {
+          Bucket b;
+          b.layer = k;
+          b.row0 = g * grows + c * rows;
+          b.rows = rows;
+          b.bias = g + 1 == ng && c + 1 == ne;
+          b.pstart = L.w_off[static_cast<size_t>(k)] + static_cast<int64_t>(b.row0) * in;
+          b.n = static_cast<int64_t>(rows) * in + (b.bias ? out : 0);
+          b.blk_rows = c == 0 ? grows : 0;
+          b.blk_bias = c == 0 && g + 1 == ng;
+          layer_buckets[static_cast<size_t>(k)].push_back(static_cast<int>(buckets.size()));
+          buckets.push_back(b);
+        }
       }
     }
     check<ConfigError>(static_cast<int>(buckets.size()) <= kMaxBuckets, "model too large: more than ", kMaxBuckets,
@@ -875,7 +890,11 @@ class RankImpl final : public Rank {
 
   // Weight gradient of bucket b (a row block of dW_k, plus db_k for the layer's last block).
   void backward_bucket(Worker& w, int b) {
-    const Bucket& bk = geo_.buckets[static_cast<size_t>(b)];
+    const Bucket& bk0 = geo_.buckets[static_cast<size_t>(b)];
+    if (bk0.blk_rows == 0) return;  // inside a block: its first bucket's GEMM wrote it
+    Bucket bk = bk0;                  // the whole block: rows, and the bias when it ends the layer
+    bk.rows = bk0.blk_rows;
+    bk.bias = bk0.blk_bias;
     const int k = bk.layer;
     const int ni = L_.in(k), no = L_.out(k);
     T* gW = w.payload + bk.poff;
@@ -883,6 +902,8 @@ class RankImpl final : public Rank {
     if (use_tc_) {
       const bool fuse = fused_scatter();
       const bool fupd = fused_update();
+      check<Error>(!(fuse || fupd) || bk.rows == bk0.rows,
+                   "fused scatter / update need one exchange bucket per weight-gradient block");
       {
         Timed tm(this, "gemm", main_);
         const BucketScatter sc = fuse ? bucket_scatter(w, b, 0) : BucketScatter{};

@@ -243,6 +243,7 @@ def test_multi_gpu_push_exchange_vs_oracle(groups, per_group, dtype, glob, n_gpu
         pytest.skip(f"needs {n} GPUs")
     if dtype == "fp32":
         monkeypatch.setenv("LSGD_B200_BUCKET_ELEMS", "20000")
+        monkeypatch.setenv("LSGD_B200_GEMM_ELEMS", "70000")  # two exchange buckets per weight-gradient GEMM
         cfg = lsgd.TrainConfig(algorithm="lsgd", n_workers=n, n_groups=groups, layer_sizes=[256, 512, 256],
                                n_samples=4096, n_features=256, n_classes=256, spread=6.0, mode="momentum",
                                local_batch=128, iterations=10, record_history=True)
@@ -269,6 +270,7 @@ def test_row_block_buckets_keep_parity(dtype, tol, monkeypatch):
     """Large layers are exchanged in row blocks (sub-buckets); force several blocks on a small model and check the
     reference iterates are unchanged (per-coordinate in fp64, norm-wise in fp32)."""
     monkeypatch.setenv("LSGD_B200_BUCKET_ELEMS", "100")
+    monkeypatch.setenv("LSGD_B200_GEMM_ELEMS", "400")  # several exchange buckets per weight-gradient GEMM block
     cfg = lsgd.TrainConfig(algorithm="lsgd", n_workers=4, n_groups=2, layer_sizes=[16, 64, 32, 4], n_samples=512,
                            n_features=16, n_classes=4, spread=6.0, mode="momentum", local_batch=8, iterations=12,
                            record_history=True)
