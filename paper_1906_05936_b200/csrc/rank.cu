@@ -49,15 +49,17 @@ Geometry::Geometry(const RunSpec& spec, int es) : esize(es) {
     Layout L(spec.layers);
     P = L.n_params;
     check<ConfigError>(L.depth() <= kMaxBuckets, "at most ", kMaxBuckets, " layers are supported");
-    // Exchange buckets are row blocks of W_k (heights a multiple of the 128-row GEMM tile): ~16M parameters with
-    // one worker per group, 64M for groups of k >= 2, whose exchange costs a scatter + reduce + global chain and
-    // flag round trips per bucket (2x2: 981k samples/s at 64M vs 925k at 16M, 927k with 16M buckets inside 64M GEMM
-    // blocks). The weight-gradient GEMM runs over blocks of consecutive buckets (LSGD_B200_GEMM_ELEMS; default: one
-    // bucket per block). LSGD_B200_BUCKET_ELEMS overrides the bucket target (tests force multi-bucket layers).
+    // Exchange buckets are row blocks of W_k (heights a multiple of the 128-row GEMM tile): 16M parameters on one
+    // GPU, 32M with one worker per group (2x1: 576k samples/s vs 561k at 16M), 64M for groups of k >= 2, whose
+    // exchange costs a scatter + reduce + global chain and flag round trips per bucket (2x2: 981k-1.03M at 64M vs
+    // 925k at 16M, 927k with 16M buckets inside 64M GEMM blocks). The weight-gradient GEMM runs over blocks of
+    // consecutive buckets (LSGD_B200_GEMM_ELEMS; default: one bucket per block). LSGD_B200_BUCKET_ELEMS overrides
+    // the bucket target (tests force multi-bucket layers).
     const int kk = spec.k();
     const char* env = std::getenv("LSGD_B200_BUCKET_ELEMS");
     const char* genv = std::getenv("LSGD_B200_GEMM_ELEMS");
-    const double kBucketElems = env ? std::max(1.0, std::atof(env)) : (kk >= 2 ? 64.0 : 16.0) * 1024 * 1024;
+    const double kDefault = (kk >= 2 ? 64.0 : (spec.N() > 1 ? 32.0 : 16.0)) * 1024 * 1024;
+    const double kBucketElems = env ? std::max(1.0, std::atof(env)) : kDefault;
     const double kGemmElems = genv ? std::max(kBucketElems, std::atof(genv)) : kBucketElems;
     layer_buckets.resize(static_cast<size_t>(L.depth()));
     // Layer 0's gradient is the last one the backward produces: its exchange + update are the step's exposed tail,
