@@ -74,6 +74,7 @@ struct EpiParams {
   int div_pow2;                        // div is a power of two: multiply by the exact reciprocal
   float div_inv;
   uint32_t probe;  // bring-up/tuning only (LSGD_TC_PROBE): 1 skip epilogue stores, 2 skip MMAs, 4 skip TMA loads
+  int kcb;         // K blocks per accumulation chunk (>= the K extent: one chunk; see the kernel comment)
   BucketScatter scat;  // weight-gradient output routed to the sub-slice owners (n = 0: plain ep.out)
   int fuse_upd;        // weight gradient: apply the update (upd) instead of storing the gradient
   FusedUpdate upd;
@@ -101,6 +102,15 @@ __device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(su32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {  // non-blocking probe
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
       : "=r"(ok)
       : "r"(su32(b)), "r"(parity)
       : "memory");
@@ -160,6 +170,30 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// 32 lanes x 32 columns of fp32 between TMEM and registers (one warp, its lane quadrant)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+      "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+      "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accum) {
@@ -353,6 +387,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int mt = ep.M / (BM * PAIR), nt = ep.N / BN;
   const int tiles = mt * nt * splits;
   const int nkb = k_per_split / BK;
+  // K chunks: the tensor pipe's fp32 accumulation does not round to nearest, so its error grows with the number of
+  // MMAs folded into one accumulator (linearly in K: 5.7e-5 norm-wise at K = 8192 against 1.1e-6 for an fp32 FMA
+  // GEMM). A tile's K runs as chunks of kcb k-blocks: chunk 0 accumulates into the tile's accumulator S, each later
+  // chunk into the other one (X), which the epilogue warps fold into S (S + X, round-to-nearest fp32, chunk order)
+  // while the next chunk's MMAs wait only for that fold. With one chunk this is the plain double-buffered tile loop.
+  const int kcb = ep.kcb > 0 && ep.kcb < nkb ? ep.kcb : nkb;
+  const int nch = (nkb + kcb - 1) / kcb;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -429,81 +470,150 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       constexpr uint32_t idesc = idesc_tf32(A_MN, B_MN, BM * PAIR);
-      uint32_t it = 0, local = 0;
+      uint32_t it = 0, local = 0, sess0 = 0, sess1 = 0;  // MMA sessions issued into accumulator 0 / 1
       for (int t = slot; t < tiles; t += nslots, ++local) {
-        const uint32_t a = local & 1u;
-        if (local >= 2) mbar_wait(&tempty_bar[a], ((local >> 1) & 1u) ^ 1u);  // epilogues drained this slot
-        tc_fence_after();
-        const uint32_t acc_tmem = tmem + a * TMEM_COLS;
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
-          mbar_wait(WS ? &xform_bar[s] : &full_bar[s], ph);
+        const uint32_t P = local & 1u;
+        for (int ch = 0; ch < nch; ++ch) {
+          // chunk 0 -> accumulator P (the tile's running sum S), chunks >= 1 -> the other one (X, folded into S)
+          const uint32_t b = ch == 0 ? P : P ^ 1u;
+          const uint32_t sess = b ? sess1 : sess0;
+          if (sess > 0) mbar_wait(&tempty_bar[b], (sess - 1u) & 1u);  // its previous contents consumed
           tc_fence_after();
-          const uint32_t st = su32(smem + s * C::STAGE_BYTES);
-          const uint32_t a_hi = st, a_lo = st + A_BYTES, b_hi = st + 2 * A_BYTES, b_lo = b_hi + C::B_BYTES;
+          const uint32_t acc_tmem = tmem + b * TMEM_COLS;
+          const int kb0 = ch * kcb, kb1 = kb0 + kcb < nkb ? kb0 + kcb : nkb;
+          for (int kb = kb0; kb < kb1; ++kb, ++it) {
+            const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
+            mbar_wait(WS ? &xform_bar[s] : &full_bar[s], ph);
+            tc_fence_after();
+            const uint32_t st = su32(smem + s * C::STAGE_BYTES);
+            const uint32_t a_hi = st, a_lo = st + A_BYTES, b_hi = st + 2 * A_BYTES, b_lo = b_hi + C::B_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            if (ep.probe & 2u) break;
-            const uint32_t accum = (kb > 0 || kk > 0) ? 1u : 0u;
-            const uint64_t dah = op_desc<A_MN>(a_hi, kk, ep), dal = op_desc<A_MN>(a_lo, kk, ep);
-            const uint64_t dbh = op_desc<B_MN>(b_hi, kk, ep), dbl = op_desc<B_MN>(b_lo, kk, ep);
-            if (PAIR == 2) {
-              mma_tf32_pair(acc_tmem, dah, dbl, idesc, accum);
-              mma_tf32_pair(acc_tmem, dal, dbh, idesc, 1u);
-              mma_tf32_pair(acc_tmem, dah, dbh, idesc, 1u);
-            } else {
-              mma_tf32(acc_tmem, dah, dbl, idesc, accum);
-              mma_tf32(acc_tmem, dal, dbh, idesc, 1u);
-              mma_tf32(acc_tmem, dah, dbh, idesc, 1u);
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              if (ep.probe & 2u) break;
+              const uint32_t accum = (kb > kb0 || kk > 0) ? 1u : 0u;
+              const uint64_t dah = op_desc<A_MN>(a_hi, kk, ep), dal = op_desc<A_MN>(a_lo, kk, ep);
+              const uint64_t dbh = op_desc<B_MN>(b_hi, kk, ep), dbl = op_desc<B_MN>(b_lo, kk, ep);
+              if (PAIR == 2) {
+                mma_tf32_pair(acc_tmem, dah, dbl, idesc, accum);
+                mma_tf32_pair(acc_tmem, dal, dbh, idesc, 1u);
+                mma_tf32_pair(acc_tmem, dah, dbh, idesc, 1u);
+              } else {
+                mma_tf32(acc_tmem, dah, dbl, idesc, accum);
+                mma_tf32(acc_tmem, dal, dbh, idesc, 1u);
+                mma_tf32(acc_tmem, dah, dbh, idesc, 1u);
+              }
             }
+            if (PAIR == 2) mma_commit_pair(&empty_bar[s]);  // stage s is free (in both CTAs) once these MMAs read it
+            else mma_commit(&empty_bar[s]);
           }
-          if (PAIR == 2) mma_commit_pair(&empty_bar[s]);  // stage s is free (in both CTAs) once these MMAs read it
-          else mma_commit(&empty_bar[s]);
+          if (PAIR == 2) mma_commit_pair(&tfull_bar[b]);  // accumulator b holds the finished chunk
+          else mma_commit(&tfull_bar[b]);
+          if (b) ++sess1;
+          else ++sess0;
         }
-        if (PAIR == 2) mma_commit_pair(&tfull_bar[a]);  // accumulator slot a holds the finished tile
-        else mma_commit(&tfull_bar[a]);
       }
     }
   } else {
     // epilogue warps 2..5 -> TMEM lane quadrant warp % 4 (this CTA's 128 rows of the tile)
     const int q = warp & 3;
-    uint32_t local = 0;
-    uint32_t xit = 0;  // WS: k-blocks transformed (same stage ring position as producer / MMA)
-    for (int t = slot; t < tiles; t += nslots, ++local) {
-      if (WS) {
-        // split this tile's raw weight tiles into the hi / lo operand slots as they land: elementwise, so the
-        // TMA swizzle (a 16 B-chunk permutation shared by all three tiles) needs no index math
-        const int tid = threadIdx.x - 64;
-        for (int kb = 0; kb < nkb; ++kb, ++xit) {
-          const uint32_t s = xit % STAGES, ph = (xit / STAGES) & 1u;
-          mbar_wait(&full_bar[s], ph);
-          uint8_t* st = smem + s * C::STAGE_BYTES;
-          const uint32_t raw = su32(st + 2 * A_BYTES + 2 * C::B_BYTES);
-          const uint32_t hi = su32(st + 2 * A_BYTES), lo = su32(st + 2 * A_BYTES + C::B_BYTES);
-          constexpr int N4 = C::B_BYTES / 16;
-          float4 v[N4 / 128];
+    uint32_t local = 0, es0 = 0, es1 = 0;  // accumulator 0 / 1 sessions waited for
+    uint32_t xit = 0, kb_end = 0;              // WS: k-blocks transformed / k-blocks up to the current chunk's end
+    // WS: split raw weight k-blocks into the hi / lo operand slots as they land, up to flat k-block `target`:
+    // elementwise, so the TMA swizzle (a 16 B-chunk permutation shared by all three tiles) needs no index math
+    auto transform_to = [&](uint32_t target) {
+      const int tid = threadIdx.x - 64;
+      for (; xit < target; ++xit) {
+        const uint32_t s = xit % STAGES, ph = (xit / STAGES) & 1u;
+        mbar_wait(&full_bar[s], ph);
+        uint8_t* st = smem + s * C::STAGE_BYTES;
+        const uint32_t raw = su32(st + 2 * A_BYTES + 2 * C::B_BYTES);
+        const uint32_t hi = su32(st + 2 * A_BYTES), lo = su32(st + 2 * A_BYTES + C::B_BYTES);
+        constexpr int N4 = C::B_BYTES / 16;
+        float4 v[N4 / 128];
 #pragma unroll
-          for (int j = 0; j < N4 / 128; ++j) v[j] = lds128(raw + 16u * (tid + 128 * j));  // all loads first
+        for (int j = 0; j < N4 / 128; ++j) v[j] = lds128(raw + 16u * (tid + 128 * j));  // all loads first
 #pragma unroll
-          for (int j = 0; j < N4 / 128; ++j) {
-            const uint32_t o = 16u * (tid + 128 * j);
-            const float4 h = make_float4(tf32_rna(v[j].x), tf32_rna(v[j].y), tf32_rna(v[j].z), tf32_rna(v[j].w));
-            sts128(hi + o, h);
-            sts128(lo + o, make_float4(tf32_rna(v[j].x - h.x), tf32_rna(v[j].y - h.y), tf32_rna(v[j].z - h.z),
-                                       tf32_rna(v[j].w - h.w)));
-          }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
-          __syncwarp();
-          if (lane == 0) {
-            const uint32_t bar = PAIR == 2 ? (su32(&xform_bar[s]) & kPeerMask) : su32(&xform_bar[s]);
-            asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
-          }
+        for (int j = 0; j < N4 / 128; ++j) {
+          const uint32_t o = 16u * (tid + 128 * j);
+          const float4 h = make_float4(tf32_rna(v[j].x), tf32_rna(v[j].y), tf32_rna(v[j].z), tf32_rna(v[j].w));
+          sts128(hi + o, h);
+          sts128(lo + o, make_float4(tf32_rna(v[j].x - h.x), tf32_rna(v[j].y - h.y), tf32_rna(v[j].z - h.z),
+                                     tf32_rna(v[j].w - h.w)));
         }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
+        __syncwarp();
+        if (lane == 0) {
+          const uint32_t bar = PAIR == 2 ? (su32(&xform_bar[s]) & kPeerMask) : su32(&xform_bar[s]);
+          asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+        }
+      }
+    };
+    auto release = [&](uint32_t b) {  // this warp is done with accumulator b (leader's barrier)
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t bar = PAIR == 2 ? (su32(&tempty_bar[b]) & kPeerMask) : su32(&tempty_bar[b]);
+        asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+      }
+    };
+    // wait for accumulator b; WS: meanwhile split the next k-blocks (up to `ahead`) as soon as each one lands, so
+    // the MMA warp finds transformed stages the moment it may continue (warp-uniform polls)
+    auto wait_full = [&](uint32_t b, uint32_t ahead) {
+      uint32_t& es = b ? es1 : es0;
+      if (WS) {
+        while (!__shfl_sync(0xffffffffu, mbar_test(&tfull_bar[b], es & 1u), 0)) {
+          if (xit < ahead && __shfl_sync(0xffffffffu, mbar_test(&full_bar[xit % STAGES], (xit / STAGES) & 1u), 0))
+            transform_to(xit + 1);
+        }
+      } else {
+        mbar_wait(&tfull_bar[b], es & 1u);
+      }
+      ++es;
+      tc_fence_after();
+    };
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    for (int t = slot; t < tiles; t += nslots, ++local) {
+      const uint32_t P = local & 1u, Q = P ^ 1u;
+      uint32_t ahead = 0;
+      for (int ch = 0; ch < nch; ++ch) {
+        const int len = kcb < nkb - ch * kcb ? kcb : nkb - ch * kcb;
+        kb_end += static_cast<uint32_t>(len);
+        const bool last = ch == nch - 1;
+        // WS: this chunk's k-blocks now; up to a ring's worth of the next chunk's (or next tile's) while its
+        // accumulator drains (their slots free up as this chunk's MMAs retire)
+        const int nl = !last ? (kcb < nkb - (ch + 1) * kcb ? kcb : nkb - (ch + 1) * kcb)
+                             : (t + nslots < tiles ? (kcb < nkb ? kcb : nkb) : 0);
+        ahead = kb_end + static_cast<uint32_t>(nl < STAGES ? nl : STAGES);
+        if (WS) transform_to(kb_end);
+        if (ch == 0) continue;
+        // fold chunk ch (accumulator Q) into the running sum S (accumulator P): S = S + X, in chunk order; the
+        // last chunk folds too, so Q is free for the next tile's first chunk while this tile's epilogue runs
+        if (ch == 1) wait_full(P, 0u);
+        wait_full(Q, ahead);
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 64) {  // 64 columns per TMEM round trip
+          uint32_t x0[32], s0[32], x1[32], s1[32];
+          const uint32_t xa = tmem + Q * TMEM_COLS + lane_off + static_cast<uint32_t>(c);
+          const uint32_t sa = tmem + P * TMEM_COLS + lane_off + static_cast<uint32_t>(c);
+          tmem_ld32(xa, x0);
+          tmem_ld32(sa, s0);
+          tmem_ld32(xa + 32, x1);
+          tmem_ld32(sa + 32, s1);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            s0[j] = __float_as_uint(__fadd_rn(__uint_as_float(s0[j]), __uint_as_float(x0[j])));
+            s1[j] = __float_as_uint(__fadd_rn(__uint_as_float(s1[j]), __uint_as_float(x1[j])));
+          }
+          tmem_st32(sa, s0);
+          tmem_st32(sa + 32, s1);
+        }
+        tmem_wait_st();
+        release(Q);
       }
       const int z = t / (mt * nt), r = t % (mt * nt);
       const int tm = kNFast ? r / nt : r % mt, tn = kNFast ? r % nt : r / mt;
       const int m0 = tm * BM * PAIR + static_cast<int>(rank) * BM, n0 = tn * BN;
-      const uint32_t a = local & 1u;
       // scalar fields in registers; the scatter table stays in (grid-constant) param space, where it is indexed
       const EpiParams e = ep;
       const bool raw = splits > 1;  // split-K: raw partial planes, the epilogue runs in splitk_reduce
@@ -532,29 +642,20 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("cp.async.commit_group;" ::: "memory");
       };
       if (fu) prefetch_wv(0);
-      mbar_wait(&tfull_bar[a], (local >> 1) & 1u);
-      tc_fence_after();
+      if (nch == 1) wait_full(P, ahead);
+      else tc_fence_after();  // S was last written by this warp's own fold (tcgen05.st, waited)
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         float4 nxt[8];
         if (fu && c + 32 < BN) prefetch_wv(c + 32);
         uint32_t rr[32];
-        const uint32_t taddr = tmem + a * TMEM_COLS + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
-            "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(rr[0]), "=r"(rr[1]), "=r"(rr[2]), "=r"(rr[3]), "=r"(rr[4]), "=r"(rr[5]), "=r"(rr[6]), "=r"(rr[7]),
-              "=r"(rr[8]), "=r"(rr[9]), "=r"(rr[10]), "=r"(rr[11]), "=r"(rr[12]), "=r"(rr[13]), "=r"(rr[14]),
-              "=r"(rr[15]), "=r"(rr[16]), "=r"(rr[17]), "=r"(rr[18]), "=r"(rr[19]), "=r"(rr[20]), "=r"(rr[21]),
-              "=r"(rr[22]), "=r"(rr[23]), "=r"(rr[24]), "=r"(rr[25]), "=r"(rr[26]), "=r"(rr[27]), "=r"(rr[28]),
-              "=r"(rr[29]), "=r"(rr[30]), "=r"(rr[31])
-            : "r"(taddr));
+        tmem_ld32(tmem + P * TMEM_COLS + lane_off + static_cast<uint32_t>(c), rr);
         const int cn = c + 32 < BN ? c + 32 : c;
         if (!fu && !raw) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) nxt[i] = epi_aux<EPI>(e, m0 + q * 32 + 4 * i + (lane >> 3), n0 + cn + ch * 4);
         }
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        tmem_wait_ld();
         if (ep.probe & 1u) continue;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -598,12 +699,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         __syncwarp();
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        const uint32_t bar = PAIR == 2 ? (su32(&tempty_bar[a]) & kPeerMask) : su32(&tempty_bar[a]);
-        asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
-      }
+      release(P);
     }
   }
   tc_fence_before();
@@ -1007,6 +1103,9 @@ GemmPlan make_plan(const OpView& a_hi, const float* a_lo, const OpView& b_hi, co
   p.ep.prefetch = 1u;
   static const uint32_t probe = std::getenv("LSGD_TC_PROBE") ? std::atoi(std::getenv("LSGD_TC_PROBE")) : 0;
   p.ep.probe = probe;
+  // accumulation chunk (K elements; LSGD_TC_KCHUNK, 0 = the whole K in one accumulator)
+  static const int kchunk = std::getenv("LSGD_TC_KCHUNK") ? std::atoi(std::getenv("LSGD_TC_KCHUNK")) : 512;
+  p.ep.kcb = kchunk > 0 ? (kchunk + BK - 1) / BK : 0;
   int ex = 0;
   p.ep.div_pow2 = (ep.div > 0.f && std::frexp(ep.div, &ex) == 0.5f) ? 1 : 0;
   p.ep.div_inv = p.ep.div_pow2 ? 1.0f / ep.div : 0.f;
