@@ -50,20 +50,21 @@ Geometry::Geometry(const RunSpec& spec, int es) : esize(es) {
     P = L.n_params;
     check<ConfigError>(L.depth() <= kMaxBuckets, "at most ", kMaxBuckets, " layers are supported");
     // Exchange buckets are row blocks of W_k (heights a multiple of the 128-row GEMM tile): 16M parameters on one
-    // GPU, 32M with one worker per group (2x1: 576k samples/s vs 561k at 16M), 64M for groups of k >= 2, whose
-    // exchange costs a scatter + reduce + global chain and flag round trips per bucket (2x2: 981k-1.03M at 64M vs
-    // 925k at 16M, 927k with 16M buckets inside 64M GEMM blocks). The weight-gradient GEMM runs over blocks of
-    // consecutive buckets (LSGD_B200_GEMM_ELEMS; default: one bucket per block). LSGD_B200_BUCKET_ELEMS overrides
-    // the bucket target (tests force multi-bucket layers).
+    // GPU, 32M with an exchange. The weight-gradient GEMM runs over blocks of consecutive buckets: one bucket per
+    // block for one worker per group (2x1: 560k samples/s vs 539k with 64M blocks, 499k with 64M buckets), 64M
+    // blocks for groups of k >= 2, whose exchange is a scatter + reduce + global chain per bucket: 32M buckets in
+    // 64M blocks pipeline that chain over the two halves of W_1 without shrinking its GEMM (2x2, A/B on one box:
+    // 944k vs 895k with 64M buckets, 916k with 32M blocks, 866k with 16M buckets; profiles/r1_buckets_ab.log).
+    // LSGD_B200_BUCKET_ELEMS / LSGD_B200_GEMM_ELEMS override both (tests force multi-bucket layers).
     const int kk = spec.k();
     const char* env = std::getenv("LSGD_B200_BUCKET_ELEMS");
     const char* genv = std::getenv("LSGD_B200_GEMM_ELEMS");
-    const double kDefault = (kk >= 2 ? 64.0 : (spec.N() > 1 ? 32.0 : 16.0)) * 1024 * 1024;
-    const double kBucketElems = env ? std::max(1.0, std::atof(env)) : kDefault;
-    const double kGemmElems = genv ? std::max(kBucketElems, std::atof(genv)) : kBucketElems;
+    const double kMi = 1024.0 * 1024.0;
+    const double kBucketElems = env ? std::max(1.0, std::atof(env)) : (spec.N() > 1 ? 32.0 : 16.0) * kMi;
+    const double kGemmElems = std::max(kBucketElems, genv ? std::atof(genv) : (kk >= 2 ? 64.0 * kMi : 0.0));
     layer_buckets.resize(static_cast<size_t>(L.depth()));
-    // Layer 0's gradient is the last one the backward produces: its exchange + update are the step's exposed tail,
-    // so with an exchange (N > 1) it is cut into blocks of half the size.
+    // Layer 0's gradient is the first one the backward produces and the first one the next forward needs: with an
+    // exchange (N > 1) it is cut into buckets / blocks of half the size, so its chain starts earlier.
     const bool tail_half = spec.N() > 1;
     auto split_rows = [](int out, double elems, int in) {  // divisor of out, rows a multiple of the tile quantum
       int nc = std::max(1, static_cast<int>(std::ceil(static_cast<double>(in) * out / elems)));
