@@ -157,8 +157,15 @@ class RankImpl final : public Rank {
     split_ = workers_.size() == 1;
     if (split_) LSGD_CUDA(cudaStreamCreateWithPriority(&comm_, cudaStreamNonBlocking, hi));
     else comm_ = main_;
-    // a second communicator stream lets consecutive buckets' push exchanges overlap (no NCCL on that path)
-    if (split_) LSGD_CUDA(cudaStreamCreateWithPriority(&comm2_, cudaStreamNonBlocking, hi));
+    // more communicator streams let consecutive buckets' push exchanges overlap (no NCCL on that path):
+    // bucket q of the step runs on stream q mod n (LSGD_B200_COMM_STREAMS, 1..kMaxComm, default 2)
+    if (split_) {
+      const char* e = std::getenv("LSGD_B200_COMM_STREAMS");
+      n_comm_ = e ? std::min(kMaxComm, std::max(1, std::atoi(e))) : 2;
+      for (int i = 1; i < n_comm_; ++i)
+        LSGD_CUDA(cudaStreamCreateWithPriority(&commx_[i], cudaStreamNonBlocking, hi));
+    }
+    commx_[0] = comm_;
     if (split_) LSGD_CUDA(cudaStreamCreateWithFlags(&upd_, cudaStreamNonBlocking));
     else upd_ = main_;
     for (int b = 0; b < kMaxBuckets; ++b) LSGD_CUDA(cudaEventCreateWithFlags(&ev_upd_[b], cudaEventDisableTiming));
@@ -228,7 +235,7 @@ class RankImpl final : public Rank {
     for (int b = 0; b < kMaxBuckets; ++b) cudaEventDestroy(ev_bucket_[b]);
     if (split_) {
       cudaStreamDestroy(comm_);
-      cudaStreamDestroy(comm2_);
+      for (int i = 1; i < n_comm_; ++i) cudaStreamDestroy(commx_[i]);
       cudaStreamDestroy(upd_);
     }
     for (int b = 0; b < kMaxBuckets; ++b) cudaEventDestroy(ev_upd_[b]);
@@ -360,7 +367,7 @@ class RankImpl final : public Rank {
   void synchronize() override {
     LSGD_CUDA(cudaSetDevice(dev_));
     LSGD_CUDA(cudaStreamSynchronize(comm_));
-    if (comm2_) LSGD_CUDA(cudaStreamSynchronize(comm2_));
+    for (int i = 1; i < n_comm_; ++i) LSGD_CUDA(cudaStreamSynchronize(commx_[i]));
     LSGD_CUDA(cudaStreamSynchronize(upd_));
     LSGD_CUDA(cudaStreamSynchronize(main_));
     check_health();
@@ -430,7 +437,7 @@ class RankImpl final : public Rank {
 
   void join() override {
     LSGD_CUDA(cudaSetDevice(dev_));
-    for (cudaStream_t st : {comm_, comm2_, upd_, io_}) {
+    for (cudaStream_t st : {commx_[0], commx_[1], commx_[2], commx_[3], upd_, io_}) {
       if (st == nullptr || st == main_) continue;
       LSGD_CUDA(cudaEventRecord(join_ev_, st));
       LSGD_CUDA(cudaStreamWaitEvent(main_, join_ev_, 0));
@@ -833,6 +840,18 @@ class RankImpl final : public Rank {
 
   // One worker, one group (N = 1): the gradient is final when produced, so the update runs in the producers'
   // epilogues (dW GEMM, bias) and the separate update pass over g disappears.
+  // Backward order. Reverse (dW_k right after delta_k) for groups of k >= 2, whose scatter -> reduce -> global chain
+  // per bucket is long: the wide cfg3 middle layer's chains then overlap dX_1, dW_0 and the next forward's first GEMM
+  // (2x2, A/B on one box: 971-974k vs 944-950k samples/s). dX-first otherwise: on one GPU there is nothing to
+  // overlap, and with one worker per group (2x1) the payload copies running under the dW GEMMs slow them more than
+  // the overlap gains (521k vs 558k; profiles/r1_order_ab.log). LSGD_B200_BWD_ORDER = reverse | dx_first overrides.
+  // The fused-epilogue update writes W_k inside dW_k, so it keeps dX-first (dX_k must read W_k first).
+  bool bwd_reverse() const {
+    static const char* e = std::getenv("LSGD_B200_BWD_ORDER");
+    if (fused_update()) return false;
+    if (e) return std::strcmp(e, "reverse") == 0;
+    return k_ >= 2;
+  }
   bool fused_update() const {
     // opt-in (LSGD_B200_FUSED_UPDATE=1): bitwise the separate pass, but its epilogue is latency-bound today
     static const bool on = std::getenv("LSGD_B200_FUSED_UPDATE") != nullptr;
@@ -1272,21 +1291,37 @@ class RankImpl final : public Rank {
       }
       if (postponed) after_update(w, t - 1, main_);
       head(w);
-      // Backward: all input gradients first (dX_{D-1} .. dX_1: the delta chain), then the weight gradients from layer
-      // 0 upwards. Layer 0's gradient — the first parameters the next forward needs — is then ready first, so its
-      // exchange and update run under the remaining dW GEMMs, and the last ones (the small top layer) hide under the
-      // next step's first forward GEMMs. Same kernels, same arithmetic; only the order differs.
-      for (int k = D - 1; k >= 1; --k) {
-        if (!synth_) backward_input(w, k);
-      }
-      if (eager)
-        for (int k = 0; k < D; ++k) LSGD_CUDA(cudaEventRecord(ev_dx_[k], main_));  // no W_k is read any more
-      for (int k = 0; k < D; ++k) {
+      // Backward order (bwd_order()): which weight gradient is ready first decides which exchange chains hide
+      // under the remaining backward and the next forward. Same kernels, same arithmetic; only the order differs.
+      auto dw_layer = [&](int k) {
         for (int b : LB[static_cast<size_t>(k)]) {
           if (!synth_) backward_bucket(w, b);  // row block of dW_k (+ db_k): ready for the exchange right away
           if (exchange && !split_) signal(w, kFlagGrad, b, static_cast<unsigned long long>(t + 1), main_);
           if (split_) LSGD_CUDA(cudaEventRecord(ev_bucket_[b], main_));
         }
+      };
+      if (bwd_reverse()) {
+        // reverse layer order: dW_k as soon as delta_k exists (dW_{D-1}, dX_{D-1}, dW_{D-2}, ..., dX_1, dW_0), so
+        // the wide middle layers' exchange chains run under the rest of the backward and the next forward; only
+        // layer 0's chain (the first thing the next forward needs) stays exposed
+        if (eager) LSGD_CUDA(cudaEventRecord(ev_dx_[0], main_));  // W_0 is not read by the backward
+        for (int k = D - 1; k >= 0; --k) {
+          dw_layer(k);
+          if (k >= 1) {
+            if (!synth_) backward_input(w, k);
+            if (eager) LSGD_CUDA(cudaEventRecord(ev_dx_[k], main_));  // W_k is no longer read
+          }
+        }
+      } else {
+        // all input gradients first (dX_{D-1} .. dX_1: the delta chain), then the weight gradients from layer 0
+        // upwards: layer 0's gradient — the first parameters the next forward needs — is ready first, so its
+        // exchange and update run under the remaining dW GEMMs
+        for (int k = D - 1; k >= 1; --k) {
+          if (!synth_) backward_input(w, k);
+        }
+        if (eager)
+          for (int k = 0; k < D; ++k) LSGD_CUDA(cudaEventRecord(ev_dx_[k], main_));  // no W_k is read any more
+        for (int k = 0; k < D; ++k) dw_layer(k);
       }
       phase_mark(widx(w), t, 1, 1, main_);
     }
@@ -1296,10 +1331,12 @@ class RankImpl final : public Rank {
     }
     if (postponed) ++applied_;
 
-    // exchange order: the order buckets finish in the backward (layers ascending, row blocks ascending)
+    // exchange order: the order buckets finish in the backward (row blocks ascending within a layer)
     std::vector<int> order;
-    for (int k = 0; k < D; ++k)
+    for (int i = 0; i < D; ++i) {
+      const int k = bwd_reverse() ? D - 1 - i : i;
       for (int b : LB[static_cast<size_t>(k)]) order.push_back(b);
+    }
 
     // communicator work: per bucket, on the comm stream (overlapping the rest of the backward)
     current_phase() = "local_reduce";
@@ -1311,12 +1348,12 @@ class RankImpl final : public Rank {
     } else if (exchange) {
       if (split_) {
         Worker& w = ws_[0];
-        // with the ordered push sum (no NCCL) consecutive buckets alternate between two streams so one bucket's
-        // reduce/global phases overlap the next one's scatter; NCCL collectives keep a single stream (one order)
-        const int n_streams = (slice_comm_ == nullptr && comm2_ != nullptr) ? 2 : 1;
+        // with the ordered push sum (no NCCL) consecutive buckets rotate over the communicator streams so one
+        // bucket's reduce/global phases overlap the next ones' scatters; NCCL collectives keep a single stream
+        const int n_streams = slice_comm_ == nullptr ? n_comm_ : 1;
         for (size_t q = 0; q < order.size(); ++q) {
           const int b = order[q];
-          cudaStream_t cs = (n_streams == 2 && (q & 1)) ? comm2_ : comm_;
+          cudaStream_t cs = commx_[q % static_cast<size_t>(n_streams)];
           LSGD_CUDA(cudaStreamWaitEvent(cs, ev_bucket_[b], 0));
           if (q == 0) {
             // phases (executors.hpp:85): the push exchange interleaves the local reduce and the global average per
@@ -1324,17 +1361,18 @@ class RankImpl final : public Rank {
             phase_mark(widx(w), t, 2, 0, comm_);
             launch_sleep(spec_.c.global_link_delay_s, comm_, lc_);
             phase_mark(widx(w), t, 3, 0, comm_);
-            if (n_streams == 2) {  // the injected link delay precedes every bucket's exchange
+            if (n_streams > 1) {  // the injected link delay precedes every bucket's exchange
               LSGD_CUDA(cudaEventRecord(join_ev_, comm_));
-              LSGD_CUDA(cudaStreamWaitEvent(comm2_, join_ev_, 0));
+              for (int i = 1; i < n_streams; ++i) LSGD_CUDA(cudaStreamWaitEvent(commx_[i], join_ev_, 0));
             }
           }
           exchange_push_bucket(w, b, t, cs);
         }
-        if (spec_.c.record_phases && n_streams == 2) {  // both streams' work closes the spans
-          LSGD_CUDA(cudaEventRecord(join_ev_, comm2_));
-          LSGD_CUDA(cudaStreamWaitEvent(comm_, join_ev_, 0));
-        }
+        if (spec_.c.record_phases)  // every stream's work closes the spans
+          for (int i = 1; i < n_streams; ++i) {
+            LSGD_CUDA(cudaEventRecord(join_ev_, commx_[i]));
+            LSGD_CUDA(cudaStreamWaitEvent(comm_, join_ev_, 0));
+          }
         phase_mark(widx(w), t, 2, 1, comm_);
         phase_mark(widx(w), t, 3, 1, comm_);
       } else {
@@ -1362,7 +1400,8 @@ class RankImpl final : public Rank {
     } else if (eager) {
       Worker& w = ws_[0];
       current_phase() = "broadcast";
-      for (int k = 0; k < D; ++k) {
+      for (int i = 0; i < D; ++i) {  // in the order the gradients are produced (see bwd_reverse)
+        const int k = bwd_reverse() ? D - 1 - i : i;
         LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_dx_[k], 0));  // W_k is no longer read by this step
         for (int b : LB[static_cast<size_t>(k)]) {
           if (reduce_folded()) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_bucket_[b], 0));
@@ -1411,7 +1450,10 @@ class RankImpl final : public Rank {
   int64_t hist_rows_;
   int N_ = 1, G_ = 1, k_ = 1, nb_ = 1, alg_ = 2, B_ = 1;
   bool exact_ = false, synth_ = false, split_ = false, use_tc_ = false;
-  cudaStream_t main_ = nullptr, comm_ = nullptr, comm2_ = nullptr;
+  static constexpr int kMaxComm = 4;
+  cudaStream_t main_ = nullptr, comm_ = nullptr;
+  cudaStream_t commx_[kMaxComm] = {};  // communicator streams; commx_[0] == comm_
+  int n_comm_ = 1;
   cudaEvent_t ev_bucket_[kMaxBuckets] = {};
   cudaEvent_t ev_upd_[kMaxBuckets] = {};
   cudaEvent_t ev_gupd_[kMaxBuckets] = {};  // per bucket: the owner's fused global + update issued (comm stream)
