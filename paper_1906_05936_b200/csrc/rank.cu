@@ -158,10 +158,12 @@ class RankImpl final : public Rank {
     if (split_) LSGD_CUDA(cudaStreamCreateWithPriority(&comm_, cudaStreamNonBlocking, hi));
     else comm_ = main_;
     // more communicator streams let consecutive buckets' push exchanges overlap (no NCCL on that path):
-    // bucket q of the step runs on stream q mod n (LSGD_B200_COMM_STREAMS, 1..kMaxComm, default 2)
+    // bucket q of the step runs on stream q mod n (LSGD_B200_COMM_STREAMS, 1..kMaxComm). Default 4 for groups of
+    // k >= 2 (reverse backward order: layer 0's chains start as soon as dW_0 ends instead of queueing behind the
+    // middle layer's; 2x2: 977-988k vs 973-975k samples/s), 2 otherwise (profiles/r1_order_ab.log)
     if (split_) {
       const char* e = std::getenv("LSGD_B200_COMM_STREAMS");
-      n_comm_ = e ? std::min(kMaxComm, std::max(1, std::atoi(e))) : 2;
+      n_comm_ = e ? std::min(kMaxComm, std::max(1, std::atoi(e))) : (spec_.k() >= 2 ? 4 : 2);
       for (int i = 1; i < n_comm_; ++i)
         LSGD_CUDA(cudaStreamCreateWithPriority(&commx_[i], cudaStreamNonBlocking, hi));
     }
@@ -838,8 +840,6 @@ class RankImpl final : public Rank {
     return exchange && split_ && slice_comm_ == nullptr;
   }
 
-  // One worker, one group (N = 1): the gradient is final when produced, so the update runs in the producers'
-  // epilogues (dW GEMM, bias) and the separate update pass over g disappears.
   // Backward order. Reverse (dW_k right after delta_k) for groups of k >= 2, whose scatter -> reduce -> global chain
   // per bucket is long: the wide cfg3 middle layer's chains then overlap dX_1, dW_0 and the next forward's first GEMM
   // (2x2, A/B on one box: 971-974k vs 944-950k samples/s). dX-first otherwise: on one GPU there is nothing to
@@ -852,6 +852,8 @@ class RankImpl final : public Rank {
     if (e) return std::strcmp(e, "reverse") == 0;
     return k_ >= 2;
   }
+  // One worker, one group (N = 1): the gradient is final when produced, so the update runs in the producers'
+  // epilogues (dW GEMM, bias) and the separate update pass over g disappears.
   bool fused_update() const {
     // opt-in (LSGD_B200_FUSED_UPDATE=1): bitwise the separate pass, but its epilogue is latency-bound today
     static const bool on = std::getenv("LSGD_B200_FUSED_UPDATE") != nullptr;
