@@ -174,6 +174,10 @@ class RankImpl final : public Rank {
     for (int b = 0; b < kMaxBuckets; ++b) LSGD_CUDA(cudaEventCreateWithFlags(&ev_dx_[b], cudaEventDisableTiming));
     for (int b = 0; b < kMaxBuckets; ++b) LSGD_CUDA(cudaEventCreateWithFlags(&ev_gupd_[b], cudaEventDisableTiming));
     for (int b = 0; b < kMaxBuckets; ++b) LSGD_CUDA(cudaEventCreateWithFlags(&ev_bucket_[b], cudaEventDisableTiming));
+    for (int b = 0; b < kMaxBuckets; ++b) LSGD_CUDA(cudaEventCreateWithFlags(&ev_bias_[b], cudaEventDisableTiming));
+    LSGD_CUDA(cudaEventCreateWithFlags(&ev_bias_src_, cudaEventDisableTiming));
+    const char* be = std::getenv("LSGD_B200_BIAS_STREAM");  // 0: bias gradients on the main stream (A/B only)
+    if (split_ && !(be && std::atoi(be) == 0)) LSGD_CUDA(cudaStreamCreateWithPriority(&bias_, cudaStreamNonBlocking, hi));
     LSGD_CUDA(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming));
     void* to = nullptr;
     LSGD_CUDA(cudaHostAlloc(&to, sizeof(int), cudaHostAllocMapped));
@@ -235,6 +239,9 @@ class RankImpl final : public Rank {
     cudaFree(bad_dev_);
     for (int i = 0; i < kRing; ++i) cudaEventDestroy(ring_ev_[i]);
     for (int b = 0; b < kMaxBuckets; ++b) cudaEventDestroy(ev_bucket_[b]);
+    for (int b = 0; b < kMaxBuckets; ++b) cudaEventDestroy(ev_bias_[b]);
+    cudaEventDestroy(ev_bias_src_);
+    if (bias_) cudaStreamDestroy(bias_);
     if (split_) {
       cudaStreamDestroy(comm_);
       for (int i = 1; i < n_comm_; ++i) cudaStreamDestroy(commx_[i]);
@@ -371,6 +378,7 @@ class RankImpl final : public Rank {
     LSGD_CUDA(cudaStreamSynchronize(comm_));
     for (int i = 1; i < n_comm_; ++i) LSGD_CUDA(cudaStreamSynchronize(commx_[i]));
     LSGD_CUDA(cudaStreamSynchronize(upd_));
+    if (bias_) LSGD_CUDA(cudaStreamSynchronize(bias_));
     LSGD_CUDA(cudaStreamSynchronize(main_));
     check_health();
     unsigned bad = 0;
@@ -439,7 +447,7 @@ class RankImpl final : public Rank {
 
   void join() override {
     LSGD_CUDA(cudaSetDevice(dev_));
-    for (cudaStream_t st : {commx_[0], commx_[1], commx_[2], commx_[3], upd_, io_}) {
+    for (cudaStream_t st : {commx_[0], commx_[1], commx_[2], commx_[3], upd_, io_, bias_}) {
       if (st == nullptr || st == main_) continue;
       LSGD_CUDA(cudaEventRecord(join_ev_, st));
       LSGD_CUDA(cudaStreamWaitEvent(main_, join_ev_, 0));
@@ -928,6 +936,20 @@ class RankImpl final : public Rank {
       const bool fupd = fused_update();
       check<Error>(!(fuse || fupd) || bk.rows == bk0.rows,
                    "fused scatter / update need one exchange bucket per weight-gradient block");
+      // the layer's bias gradient belongs to its last bucket (the block that ends the layer computes it)
+      const int bb = bk.bias ? geo_.layer_buckets[static_cast<size_t>(k)].back() : b;
+      bias_side_[bb] = bk.bias && bias_ && !fuse && !fupd && alg_ == LSGD_B200_LSGD && !flat_nccl();
+      if (bias_side_[bb]) {
+        // db_k = colsum(delta_k) / B needs none of the dW GEMM's results: it runs on the bias stream beside it
+        // (the bias kernel was ~4% of the one-GPU step on the main stream); the bucket's exchange / update wait for it
+        LSGD_CUDA(cudaEventRecord(ev_bias_src_, main_));
+        LSGD_CUDA(cudaStreamWaitEvent(bias_, ev_bias_src_, 0));
+        {
+          Timed tb(this, "bias", bias_);
+          tc_backward_bias(w.tc, L_, k, reinterpret_cast<float*>(gb), bias_, lc_, nullptr, nullptr);
+        }
+        LSGD_CUDA(cudaEventRecord(ev_bias_[bb], bias_));
+      }
       {
         Timed tm(this, "gemm", main_);
         const BucketScatter sc = fuse ? bucket_scatter(w, b, 0) : BucketScatter{};
@@ -935,7 +957,7 @@ class RankImpl final : public Rank {
         tc_backward_dw(w.tc, L_, k, bk.row0, bk.rows, reinterpret_cast<float*>(gW), main_, lc_, fuse ? &sc : nullptr,
                        fupd ? &fu : nullptr);
       }
-      if (bk.bias) {
+      if (bk.bias && !bias_side_[bb]) {
         Timed tb(this, "bias", main_);
         const BucketScatter sc = fuse ? bucket_scatter(w, b, static_cast<int64_t>(bk.rows) * ni) : BucketScatter{};
         const FusedUpdate fu =
@@ -1292,6 +1314,11 @@ class RankImpl final : public Rank {
         forward_layer(w, k);
       }
       if (postponed) after_update(w, t - 1, main_);
+      // the previous step's side-stream bias gradients read the deltas this step's backward rewrites
+      if (bias_) {
+        LSGD_CUDA(cudaEventRecord(ev_bias_src_, bias_));
+        LSGD_CUDA(cudaStreamWaitEvent(main_, ev_bias_src_, 0));
+      }
       head(w);
       // Backward order (bwd_order()): which weight gradient is ready first decides which exchange chains hide
       // under the remaining backward and the next forward. Same kernels, same arithmetic; only the order differs.
@@ -1357,6 +1384,7 @@ class RankImpl final : public Rank {
           const int b = order[q];
           cudaStream_t cs = commx_[q % static_cast<size_t>(n_streams)];
           LSGD_CUDA(cudaStreamWaitEvent(cs, ev_bucket_[b], 0));
+          if (bias_side_[b]) LSGD_CUDA(cudaStreamWaitEvent(cs, ev_bias_[b], 0));
           if (q == 0) {
             // phases (executors.hpp:85): the push exchange interleaves the local reduce and the global average per
             // bucket, so local_reduce spans the whole exchange and global_allreduce starts after the link delay
@@ -1407,6 +1435,7 @@ class RankImpl final : public Rank {
         LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_dx_[k], 0));  // W_k is no longer read by this step
         for (int b : LB[static_cast<size_t>(k)]) {
           if (reduce_folded()) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_bucket_[b], 0));
+          if (reduce_folded() && bias_side_[b]) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_bias_[b], 0));
           apply_bucket(w, b, t, upd_);
           if (own_slot_fused()) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_gupd_[b], 0));  // own slot (comm stream)
           LSGD_CUDA(cudaEventRecord(ev_upd_[b], upd_));
@@ -1457,6 +1486,11 @@ class RankImpl final : public Rank {
   cudaStream_t commx_[kMaxComm] = {};  // communicator streams; commx_[0] == comm_
   int n_comm_ = 1;
   cudaEvent_t ev_bucket_[kMaxBuckets] = {};
+  // bias gradient of a layer on its own stream (off the GEMM chain): consumers of bucket b also wait ev_bias_[b]
+  cudaStream_t bias_ = nullptr;
+  cudaEvent_t ev_bias_[kMaxBuckets] = {};
+  cudaEvent_t ev_bias_src_ = nullptr;
+  bool bias_side_[kMaxBuckets] = {};
   cudaEvent_t ev_upd_[kMaxBuckets] = {};
   cudaEvent_t ev_gupd_[kMaxBuckets] = {};  // per bucket: the owner's fused global + update issued (comm stream)
   cudaEvent_t ev_dx_[kMaxBuckets] = {};
