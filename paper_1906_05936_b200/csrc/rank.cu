@@ -66,6 +66,8 @@ Geometry::Geometry(const RunSpec& spec, int es) : esize(es) {
     // Layer 0's gradient is the first one the backward produces and the first one the next forward needs: with an
     // exchange (N > 1) it is cut into buckets / blocks of half the size, so its chain starts earlier.
     const bool tail_half = spec.N() > 1;
+    const char* l0env = std::getenv("LSGD_B200_L0_DIV");  // layer-0 bucket / block divisor with an exchange (A/B)
+    const double l0div = l0env ? std::max(1.0, std::atof(l0env)) : 2.0;
     auto split_rows = [](int out, double elems, int in) {  // divisor of out, rows a multiple of the tile quantum
       int nc = std::max(1, static_cast<int>(std::ceil(static_cast<double>(in) * out / elems)));
       const int quantum = out % 128 == 0 ? 128 : (out % 8 == 0 ? 8 : out);
@@ -74,8 +76,8 @@ Geometry::Geometry(const RunSpec& spec, int es) : esize(es) {
     };
     for (int k = 0; k < L.depth(); ++k) {
       const int in = L.in(k), out = L.out(k);
-      const double btarget = (k == 0 && tail_half) ? kBucketElems / 2 : kBucketElems;
-      const double gtarget = (k == 0 && tail_half) ? kGemmElems / 2 : kGemmElems;
+      const double btarget = (k == 0 && tail_half) ? kBucketElems / l0div : kBucketElems;
+      const double gtarget = (k == 0 && tail_half) ? kGemmElems / l0div : kGemmElems;
       const int ng = split_rows(out, gtarget, in), grows = out / ng;
       for (int g = 0; g < ng; ++g) {
         int ne = split_rows(grows, btarget, in);
