@@ -1,0 +1,107 @@
+"""One process per GPU through the rank API (lsgd_b200_rank_create -> export -> connect over a gloo allgather ->
+step -> drain), the way bench.py / torchrun drive it (run_rank seam, executors.hpp:143-144): the final parameters
+match the oracle (fp64 per coordinate, fp32 tensor-core path norm-wise) and agree bitwise across ranks, and a peer
+that never arrives surfaces as TransportError (the collective timeout of transport.cpp / tcp.cpp) instead of a hang.
+"""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _cfg(dtype, n, groups):
+    import paper_1906_05936_b200 as lsgd
+    if dtype == "fp64":
+        cfg = lsgd.TrainConfig(algorithm="lsgd", n_workers=n, n_groups=groups, layer_sizes=[16, 24, 8], n_samples=512,
+                               n_features=16, n_classes=8, spread=6.0, mode="momentum", local_batch=8, iterations=12)
+    else:  # tensor-core-eligible: the production schedule (buckets, streams, backward order of the layout)
+        cfg = lsgd.TrainConfig(algorithm="lsgd", n_workers=n, n_groups=groups, layer_sizes=[256, 512, 256],
+                               n_samples=4096, n_features=256, n_classes=256, spread=6.0, mode="momentum",
+                               local_batch=128, iterations=10)
+    cfg.b200.dtype = dtype
+    return cfg
+
+
+def _worker(rank, world, port, dtype, groups, mode, out):
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import paper_1906_05936_b200 as lsgd
+    from paper_1906_05936_b200.executors import Rank
+
+    torch.cuda.set_device(rank)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = _cfg(dtype, world, groups)
+        if mode == "timeout":
+            cfg.collective_timeout_s = 2.0
+        r = Rank(cfg, rank, rank)
+        blobs = [None] * world
+        dist.all_gather_object(blobs, r.export())
+        r.connect(blobs)
+        r.synchronize()
+        if mode == "train":
+            r.step(cfg.iterations)
+            r.drain()
+            out[rank] = r.params()
+        elif rank == 0:  # rank 1 never steps: every flag rank 0 waits for stays unset
+            try:
+                r.step(1)
+                r.synchronize()
+                out["err"] = None
+            except lsgd.LsgdError as e:
+                out["err"] = type(e).__name__
+        dist.barrier()
+        r.close()
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def _spawn(world, dtype, groups, mode):
+    import torch.multiprocessing as mp
+    mgr = mp.get_context("spawn").Manager()  # no fork() of this multi-threaded process
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), dtype, groups, mode, out), nprocs=world, join=True)
+    return dict(out)
+
+
+@pytest.mark.parametrize("groups,per_group,dtype", [(2, 1, "fp64"), (2, 2, "fp64"), (1, 2, "fp64"), (2, 2, "fp32")])
+def test_process_per_gpu_ranks_match_oracle(groups, per_group, dtype, n_gpus):
+    n = groups * per_group
+    if n_gpus < n:
+        pytest.skip(f"needs {n} GPUs")
+    out = _spawn(n, dtype, groups, "train")
+    from oracle import Oracle, TrainSpec
+    cfg = _cfg(dtype, n, groups)
+    spec = TrainSpec(**{k: getattr(cfg, k) for k in TrainSpec.__dataclass_fields__ if hasattr(cfg, k)})
+    ref = Oracle("port").run_train(spec)["final_params"]
+    w0 = out[0]
+    if dtype == "fp64":
+        rel = np.abs(w0 - ref) / np.maximum(np.abs(ref), 1e-8)
+        assert rel.max() <= 1e-8, rel.max()
+    else:
+        dev = np.linalg.norm(w0 - ref) / np.linalg.norm(ref)
+        assert dev <= 1e-5, dev
+    for q in range(1, n):  # every replica holds the same bits
+        assert np.array_equal(out[q].view(np.uint64), w0.view(np.uint64))
+
+
+def test_missing_peer_is_a_transport_error_not_a_hang(n_gpus):
+    if n_gpus < 2:
+        pytest.skip("needs 2 GPUs")
+    out = _spawn(2, "fp64", 2, "timeout")
+    assert out["err"] == "TransportError", out
