@@ -35,10 +35,12 @@ METRIC = "samples/sec (LSGD step, weak scaling, B_loc per GPU)"
 UNIT = "samples/s"
 
 
-def workload(name: str, n: int, bloc: int | None, algo: str, glob: str = "ordered"):
+def workload(name: str, n: int, bloc: int | None, algo: str, glob: str = "ordered", groups: int | None = None):
     import paper_1906_05936_b200 as lsgd
 
-    G = min(2, n) if algo == "lsgd" else 1
+    G = (groups or min(2, n)) if algo == "lsgd" else 1
+    if n % G:
+        raise SystemExit(f"--groups {G} does not divide {n} workers")
     if name == "cfg3":
         layers = [4096, 8192, 8192, 512]
         cfg = lsgd.TrainConfig(algorithm=algo, n_workers=n, n_groups=G, layer_sizes=layers, n_samples=65536,
@@ -128,7 +130,8 @@ def dist_env():
 
 
 # ------------------------------------------------------------------------------------------------ reference arm
-def cpu_reference(cfg_name: str, n: int, steps: int, warmup: int, bloc: int | None, algo: str):
+def cpu_reference(cfg_name: str, n: int, steps: int, warmup: int, bloc: int | None, algo: str,
+                  groups: int | None = None):
     """The reference's own run_train (UNMODIFIED sources, oracle/_ref) timed on the host cores."""
     from oracle import Oracle, TrainSpec
 
@@ -143,14 +146,14 @@ def cpu_reference(cfg_name: str, n: int, steps: int, warmup: int, bloc: int | No
         # the reference's per-sample cost does not depend on the batch or dataset size
         b = max(1, min(8, cores // max(1, n)))
         iters = max(1, min(steps, 3))
-        spec = TrainSpec(algorithm=algo, n_workers=n, n_groups=min(2, n) if algo == "lsgd" else 1,
+        spec = TrainSpec(algorithm=algo, n_workers=n, n_groups=(groups or min(2, n)) if algo == "lsgd" else 1,
                          layer_sizes=[4096, 8192, 8192, 512], n_samples=max(1024, 4 * b * n), n_features=4096,
                          n_classes=512, mode="momentum", local_batch=b, iterations=iters)
         sample = (f"run_train lsgd {spec.n_groups}x{n // spec.n_groups}, MLP 4096-8192-8192-512 fp64, B_loc={b}, "
                   f"{iters} iterations on {spec.n_samples} blobs (per-step cost is independent of n)")
     else:
         b = bloc or 16
-        spec = TrainSpec(algorithm=algo, n_workers=n, n_groups=min(2, n) if algo == "lsgd" else 1,
+        spec = TrainSpec(algorithm=algo, n_workers=n, n_groups=(groups or min(2, n)) if algo == "lsgd" else 1,
                          layer_sizes=[32, 16, 10], mode="momentum", local_batch=b, iterations=max(steps, 100))
         sample = f"run_train {algo} N={n}, MLP 32-16-10 fp64, B_loc={b}, {spec.iterations} iterations"
     if warmup:
@@ -165,7 +168,7 @@ def run_reference_arm(args):
     rank, _, world = dist_env()
     if rank != 0:
         return 0
-    cb = cpu_reference(args.workload, args.gpus, args.steps, args.warmup, args.bloc, args.algo)
+    cb = cpu_reference(args.workload, args.gpus, args.steps, args.warmup, args.bloc, args.algo, args.groups)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -207,7 +210,7 @@ def run_b200_arm(args):
         pg.all_gather_object(out, obj)
         return out
 
-    cfg = workload(args.workload, n, args.bloc, args.algo, args.global_allreduce)
+    cfg = workload(args.workload, n, args.bloc, args.algo, args.global_allreduce, args.groups)
     t_setup = time.time()
     r = Rank(cfg, rank, local)
     r.connect(allgather(r.export()))
@@ -372,6 +375,8 @@ def main():
     ap.add_argument("--global-allreduce", default="ordered", choices=["nccl", "ordered"],
                     help="LSGD inter-group average: NCCL over the slot owners, or the ordered push sum")
     ap.add_argument("--bloc", type=int, default=None)
+    ap.add_argument("--groups", type=int, default=None,
+                    help="LSGD communicator groups (default min(2, N): N=8 -> 2x4); e.g. 1 for 1xN, N for Nx1")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     args = ap.parse_args()
