@@ -323,14 +323,25 @@ def run_b200_arm(args):
                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (3xTF32 ceiling = peak/6)",
                     "flops_per_launch": B * F, "launches_timed": gemm_n}
         else:
-            avg, cnt = fams["update"]
-            up_ms = avg * cnt / args.steps
+            # synthetic gradient: the step is exchange + update; the roofline kernel is the update pass. With an
+            # exchange the owner's own slot is updated inside the fused global kernel, so the update kernel covers
+            # the (k-1)/k other slots; with one worker per group (k = 1) the fused global kernel does all of it.
             P = cfg.n_params
-            bytes_ = 4 * P * (5 if cfg.mode == "momentum" else 3)
+            G = cfg.n_groups
+            k = n // G
+            wv = 4 * (2 if cfg.mode == "momentum" else 1)  # w (+ v) bytes per parameter, each read and written
+            if n > 1 and k == 1:
+                fam, kname = "global", "K7+K8 global_update (ordered group sum + update, whole slot)"
+                bytes_ = P * (4 * G + 2 * wv)  # own payload + G-1 group sums read, w (+ v) read + written
+            else:
+                fam, kname = "update", "K8 update (broadcast average + momentum update)"
+                bytes_ = P * (4 + 2 * wv) * ((k - 1) / k if n > 1 else 1.0)  # average read, w (+ v) read + written
+            avg, cnt = fams[fam]
+            up_ms = avg * cnt / args.steps
             ach = bytes_ / (up_ms / 1e3) / 1e9 if up_ms else None
             peak = peaks.get("hbm_gbs") or 6650.0
             roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": (ach / peak) if ach else None,
-                    "traffic": None, "kernel": "K8 broadcast-pull + momentum update"}
+                    "traffic": None, "kernel": kname, "bytes_per_launch_step": bytes_}
         # step-level roofline of the north star: t_roof = max(B_loc*F / GEMM_peak,
         # 4(P+1) / BW_NVLink), GEMM_peak = the 3xTF32 effective rate of the measured dense peak (peak/6)
         step_roof = None
