@@ -162,10 +162,11 @@ class RankImpl final : public Rank {
     // more communicator streams let consecutive buckets' push exchanges overlap (no NCCL on that path):
     // bucket q of the step runs on stream q mod n (LSGD_B200_COMM_STREAMS, 1..kMaxComm). Default 4 for groups of
     // k >= 2 (reverse backward order: layer 0's chains start as soon as dW_0 ends instead of queueing behind the
-    // middle layer's; 2x2: 977-988k vs 973-975k samples/s), 2 otherwise (profiles/r1_order_ab.log)
+    // middle layer's; 2x2: 977-988k vs 973-975k samples/s), 3 otherwise (2x1: 560k vs 556k with 2;
+    // profiles/r1_order_ab.log)
     if (split_) {
       const char* e = std::getenv("LSGD_B200_COMM_STREAMS");
-      n_comm_ = e ? std::min(kMaxComm, std::max(1, std::atoi(e))) : (spec_.k() >= 2 ? 4 : 2);
+      n_comm_ = e ? std::min(kMaxComm, std::max(1, std::atoi(e))) : (spec_.k() >= 2 ? 4 : 3);
       for (int i = 1; i < n_comm_; ++i)
         LSGD_CUDA(cudaStreamCreateWithPriority(&commx_[i], cudaStreamNonBlocking, hi));
     }
