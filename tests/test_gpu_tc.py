@@ -168,6 +168,44 @@ def test_weight_split_in_shared_memory_is_bitwise_the_hbm_split():
     assert np.array_equal(ws.view(np.uint64), hbm.view(np.uint64))
 
 
+_KCHUNK_PROBE = """
+import sys, numpy as np
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+from test_gpu_tc import tc_gemm
+rng = np.random.default_rng(11)
+M, N, K = 1024, 4096, 4096  # 4 x 16 = 64 pair tiles over 64 slots, and split-free long K: 8 chunks of 512
+A = np.maximum(rng.standard_normal((M, K)), 0).astype(np.float32)  # post-ReLU activations: no sign cancellation
+B = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
+ref = A.astype(np.float64) @ B.astype(np.float64).T
+fwd = tc_gemm(A, B, 0, 0, epi=0, bias=np.zeros(N, np.float32))
+ig = tc_gemm(A, B, 0, 1, epi=2, mask=np.ones((M, N), np.float32))
+M2 = 4096  # 16 x 16 = 256 pair tiles: 4 per CTA pair, so chunk folds and tile epilogues interleave
+A2 = np.maximum(rng.standard_normal((M2, K)), 0).astype(np.float32)
+ref2 = A2.astype(np.float64) @ B.astype(np.float64).T
+fwd2 = tc_gemm(A2, B, 0, 0, epi=0, bias=np.zeros(N, np.float32))
+r = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
+np.save(sys.argv[1], np.array([r(fwd, ref), r(ig, ref), r(fwd2, ref2)]))
+"""
+
+
+@pytest.mark.parametrize("ws", ["0", "1"])
+def test_k_chunked_accumulation_is_fp32_class(ws):
+    """The tensor pipe's fp32 accumulation does not round to nearest: one accumulator over K = 4096 drifts ~1.4e-5
+    norm-wise from float64. With 512-wide K chunks folded in TMEM (default) the error stays at the one-chunk level
+    (~3.6e-6) on one-tile-per-CTA and several-tiles-per-CTA shapes, for the forward and dX forms, with the weights
+    split in shared memory (WS=1, the transform interleaved with the folds) or read pre-split from HBM."""
+    errs = {}
+    for kc in ("512", "0"):
+        with tempfile.TemporaryDirectory() as td:
+            out = os.path.join(td, "e.npy")
+            env = dict(os.environ, LSGD_TC_KCHUNK=kc, LSGD_TC_TEST_WS=ws)
+            subprocess.run([sys.executable, "-c", _KCHUNK_PROBE % (ROOT, os.path.join(ROOT, "tests")), out],
+                           check=True, env=env, cwd=ROOT)
+            errs[kc] = np.load(out)
+    assert errs["512"].max() < 6e-6, errs
+    assert (errs["0"] > 2.5 * errs["512"]).all(), errs
+
+
 def test_full_size_cfg3_steps_match_torch_fp64():
     """BASELINE cfg3 at full size (MLP 4096-8192-8192-512, 105M parameters, B_loc = 512, momentum): three steps of
     the production fp32 path (tcgen05 split-TF32 GEMMs, in-SMEM weight split, fused head, eager bucket updates) and of
