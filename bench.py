@@ -321,6 +321,7 @@ def run_b200_arm(args):
                     "traffic_unit": "bytes DRAM read+write per launch (= one step's GEMM sequence)",
                     "kernel": "forward+backward GEMM sequence per step (B_loc*F flops / its device time)",
                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (3xTF32 ceiling = peak/6)",
+                    "frac_of_3xtf32_ceiling": (ach / (peak / 6)) if ach else None,
                     "flops_per_launch": B * F, "launches_timed": gemm_n}
         else:
             # synthetic gradient: the step is exchange + update; the roofline kernel is the update pass. With an
