@@ -357,6 +357,18 @@ def run_b200_arm(args):
                          "basis": "3xTF32 = bf16_tflops_sustained/6; NVLink 900 GB/s per direction"}
         kern = {f: {"avg_ms": v[0], "count": v[1], "ms_per_step": v[0] * v[1] / args.steps}
                 for f, v in fams.items() if v[1]}
+        # exposed communication (BASELINE metric): step time not covered by the main stream's compute kernels
+        # (rank 0's per-step device time of its GEMMs, gather, head, split; the bias gradients run on their own
+        # stream under LSGD, on the main stream otherwise)
+        exposed = None
+        if cfg.b200.model == "mlp":
+            main_fams = ["gemm", "gather", "head", "split"]
+            if args.algo != "lsgd" or os.environ.get("LSGD_B200_BIAS_STREAM") == "0":
+                main_fams.append("bias")
+            main_ms = sum(kern[f]["ms_per_step"] for f in main_fams if f in kern)
+            exposed = {"ms_per_step": max(0.0, ms_max / args.steps - main_ms), "main_compute_ms": main_ms,
+                       "basis": "ms_per_step - per-step device time of the main-stream compute kernels ("
+                                + ", ".join(main_fams) + ")"}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
@@ -367,7 +379,7 @@ def run_b200_arm(args):
                            "global_allreduce": cfg.b200.global_allreduce,
                            "l2": "working set (w, v, grad, slices) >> 126 MB L2; no flush needed"},
                 "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,
-                "step_roofline": step_roof, "kernels": kern, "setup_s": setup_s}
+                "step_roofline": step_roof, "exposed_comm": exposed, "kernels": kern, "setup_s": setup_s}
         print(json.dumps(line), flush=True)
     r.close()
     if pg:
