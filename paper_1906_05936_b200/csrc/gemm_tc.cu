@@ -3,10 +3,13 @@
 // Persistent kernel, one CTA per SM, 128 x 256 fp32 tiles D = A * B^T (TN form: A is M x K, B is N x K) in TMEM:
 //   warp 0      TMA producer: per 16-wide K block, A_hi, A_lo, B_hi, B_lo -> one 48 KB smem stage (4-stage ring)
 //   warp 1      TMEM allocator + single-thread MMA issuer: per 8-wide K step three tcgen05.mma.kind::tf32
-//               (hi*lo, lo*hi, hi*hi) accumulate into one of two 256-column TMEM accumulators; tcgen05.commit
-//               frees the stage / hands the finished accumulator to the epilogue
-//   warps 2..5  epilogue (overlapping the next tile's MMAs): tcgen05.ld 32x32b -> registers -> fused bias/ReLU |
-//               /B | ReLU-mask, fp32 output plus the hi/lo split the next GEMM consumes
+//               (hi*lo, lo*hi, hi*hi) accumulate into one of two 256-column TMEM accumulators, K in chunks of
+//               512 (chunk 0 -> the tile's sum S, later chunks -> the other accumulator X); tcgen05.commit frees
+//               the stage / hands a finished chunk to the epilogue warps
+//   warps 2..5  fold each later chunk into S (S + X, round to nearest: the tensor pipe's own fp32 accumulation
+//               does not round, its error grows with K), then the epilogue (overlapping the next tile's first
+//               chunk): tcgen05.ld 32x32b -> registers -> fused bias/ReLU | /B | ReLU-mask, fp32 output plus the
+//               hi/lo split the next GEMM consumes; with WS they also split the raw weight k-blocks into hi/lo
 // Operands may be K-major ([rows][K], TMA SWIZZLE_64B / UMMA SWIZZLE_64B) or MN-major ([K][rows], TMA
 // SWIZZLE_128B_ATOM_32B / UMMA SWIZZLE_128B_BASE32B, the only MN-major layout tf32 supports), so dX (W read
 // MN-major) and dW (delta and activations read MN-major) need no transposed copies.
