@@ -1,9 +1,12 @@
 // Tensor-core path of the fp32 step: the dense-layer GEMMs as tcgen05.mma kind::tf32
 // with the split-TF32 ("3xTF32") decomposition  a*b ~= a_hi*b_lo + a_lo*b_hi + a_hi*b_hi, where
 // a_hi = rna_tf32(a), a_lo = rna_tf32(a - a_hi); the dropped a_lo*b_lo term is ~2^-22 relative, so products are
-// fp32-grade (the parity contract needs fp32 accuracy: SURVEY §7 "hard parts" 1, 6). Operands are staged by TMA
-// (SWIZZLE_128B) from pre-split hi/lo copies that their producers write (the weight split after each update, the
-// forward/backward epilogues for activations and deltas); accumulators live in TMEM.
+// fp32-grade (the parity contract needs fp32 accuracy: SURVEY §7 "hard parts" 1, 6). The tensor pipe's fp32
+// accumulation does not round to nearest, so K runs in 512-wide chunks whose TMEM partial sums are folded with
+// round-to-nearest adds (gemm_tc.cu): 3.6e-6 norm-wise vs float64 at any K instead of growing linearly with K.
+// Operands are staged by TMA from hi/lo copies their producers write (the forward/backward epilogues for
+// activations and deltas); the weights are split in shared memory by the forward / dX kernels themselves (WS).
+// Accumulators live in TMEM.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -27,8 +30,8 @@ struct TcWorkspace {
   float* x_hi = nullptr;       // [B, d]
   float* x_lo = nullptr;
   std::vector<float*> act, act_hi, act_lo;  // [B, out_k] per layer
-  // deltas [B, out_k] per layer: every dX runs before any dW (the gradient of layer 0 is ready first), so all
-  // layers' deltas are alive at once
+  // deltas [B, out_k] per layer: dX and dW interleave in either backward order (rank.cu bwd_reverse), so every
+  // layer keeps its own delta
   std::vector<float*> dlt, dlt_hi, dlt_lo;
   float* partial = nullptr;    // split-K workspace
   size_t partial_elems = 0;
@@ -36,7 +39,7 @@ struct TcWorkspace {
   bool weights_split_in_smem = false;  // the updates need not write w_hi / w_lo
 };
 
-// Every layer width a multiple of 256 and the local batch a multiple of 128 (tile 128 x 256, BK = 32).
+// Every layer width a multiple of 256 and the local batch a multiple of 128 (tile 128 x 256, BK = 16).
 bool tc_shapes_supported(const std::vector<int32_t>& layers, int batch);
 // w_master (the fp32 weights, fixed address): when given (and LSGD_TC_WSPLIT != 0) the forward and input-gradient
 // GEMMs read it raw and split it in shared memory, so w_hi / w_lo need not be kept current.
