@@ -1078,7 +1078,7 @@ GemmPlan make_plan(const OpView& a_hi, const float* a_lo, const OpView& b_hi, co
   p.K = static_cast<int>(a_hi.k);
   check<Error>(a_hi.k == b_hi.k, "gemm: K mismatch");
   check<Error>(p.M % BM == 0 && p.N % BN == 0 && p.K % BK == 0, "gemm: shape ", p.M, "x", p.N, "x", p.K,
-               " is not a multiple of the 128x256x32 tile");
+               " is not a multiple of the 128x256x16 tile");
   // CTA pairs whenever the M extent allows 256-row tiles (LSGD_TC_PAIR=0 forces single CTAs: tuning only)
   static const bool no_pair = std::getenv("LSGD_TC_PAIR") && std::atoi(std::getenv("LSGD_TC_PAIR")) == 0;
   p.pair = (!no_pair && p.M % (2 * BM) == 0) ? 2 : 1;
