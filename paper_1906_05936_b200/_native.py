@@ -1,7 +1,8 @@
 """ctypes binding of ``include/lsgd_b200.h`` (the C-ABI of ``liblsgd_b200.so``, built in-tree for sm_100a).
 
-There is no CPU fallback: importing this module fails loudly when the shared library is missing, and every
-compute entry point raises when no sm_100 device is visible.
+There is no CPU fallback: the first use of ``lib`` fails loudly when the shared library is missing, and every
+compute entry point raises when no sm_100 device is visible. The library is loaded lazily (module ``__getattr__``)
+so that ``__graft_entry__.build()`` can import the package's build helper before the library exists.
 """
 from __future__ import annotations
 
@@ -113,13 +114,27 @@ def _load():
     return lib
 
 
-lib = _load()
+_LIB = None
+
+
+def get_lib():
+    """The loaded liblsgd_b200.so (loaded on first use; ImportError when it has not been built)."""
+    global _LIB
+    if _LIB is None:
+        _LIB = _load()
+    return _LIB
+
+
+def __getattr__(name):
+    if name == "lib":
+        return get_lib()
+    raise AttributeError(name)
 
 
 def check(rc: int) -> None:
     if rc == OK:
         return
-    msg = lib.lsgd_b200_last_error().decode(errors="replace")
+    msg = get_lib().lsgd_b200_last_error().decode(errors="replace")
     raise {ERR_CONFIG: ConfigError, ERR_TRANSPORT: TransportError}.get(rc, LsgdError)(msg)
 
 
