@@ -190,8 +190,8 @@ def run_b200_arm(args):
     rank, local, world = dist_env()
     n = world if world > 1 else args.gpus
     if world == 1 and args.gpus > 1:
-        raise SystemExit("for --gpus > 1 launch with torchrun (one process per GPU)")
-    torch.cuda.set_device(local)
+        raise SystemExit("--gpus > 1 needs one process per GPU (bench.py self-launches them when WORLD_SIZE is "
+                         "unset; this rank saw WORLD_SIZE=1)")
     pg = None
     if world > 1:
         import torch.distributed as dist
@@ -212,7 +212,9 @@ def run_b200_arm(args):
 
     cfg = workload(args.workload, n, args.bloc, args.algo, args.global_allreduce, args.groups)
     t_setup = time.time()
-    r = Rank(cfg, rank, local)
+    print(f"[bench rank {rank}/{world}] creating Rank on device {local}", file=sys.stderr, flush=True)
+    r = Rank(cfg, rank, local)  # fails loudly (LsgdError / ImportError) without an sm_100 GPU or the library
+    torch.cuda.set_device(local)
     r.connect(allgather(r.export()))
     r.synchronize()
     setup_s = time.time() - t_setup
@@ -388,6 +390,40 @@ def run_b200_arm(args):
     return 0
 
 
+def self_launch(argv, n):
+    """`bench.py --gpus N` without torchrun: spawn N rank processes (one per GPU) on a 127.0.0.1 rendezvous, the
+    environment torchrun would give them; rank 0's stdout is this process's stdout. Any rank failing stops the
+    others and the job exits non-zero."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + argv, env=env,
+                                      stdout=None if r == 0 else subprocess.DEVNULL))
+    rc = 0
+    try:
+        while procs:
+            for p in list(procs):
+                c = p.poll()
+                if c is None:
+                    continue
+                procs.remove(p)
+                if c != 0:
+                    rc = rc or c
+                    for q in procs:  # the survivors would wait in a barrier forever
+                        q.terminate()
+            time.sleep(0.05)
+    finally:
+        for p in procs:
+            p.kill()
+    return rc
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -408,6 +444,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(sys.argv[1:], args.gpus)
     return run_b200_arm(args)
 
 

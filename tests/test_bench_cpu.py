@@ -30,3 +30,17 @@ def test_csgd_is_flat_and_bad_layouts_are_rejected():
 def test_synthetic_gradient_workload():
     cfg = bench.workload("cfg4", 4, None, "lsgd")
     assert cfg.b200.model == "synthetic_gradient" and cfg.b200.synthetic_params == 25_600_000
+
+
+def test_gpus_n_self_launches_one_process_per_rank():
+    """`bench.py --gpus 2` without torchrun spawns 2 ranks that rendezvous (gloo, 127.0.0.1) and reach Rank(...);
+    without a GPU each rank fails loudly and the job exits non-zero (no CPU fallback)."""
+    import subprocess
+
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1",
+                        "--skip-cpu", "--skip-e2e"], env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode != 0
+    for r in range(2):
+        assert f"[bench rank {r}/2] creating Rank" in p.stderr, p.stderr[-3000:]
+    assert p.stdout.strip() == ""  # no bench line without a GPU
