@@ -496,11 +496,23 @@ __global__ void __launch_bounds__(256) copy_pairs_kernel(const __grid_constant__
   }
 }
 
+template <typename T>
+__device__ __forceinline__ UpdateArgs<T> gu_split_args(const GlobalUpdateArgs<T>&) {
+  return UpdateArgs<T>{};
+}
+template <>
+__device__ __forceinline__ UpdateArgs<float> gu_split_args<float>(const GlobalUpdateArgs<float>& a) {
+  UpdateArgs<float> u{};
+  u.w_hi = a.w_hi;
+  u.w_lo = a.w_lo;
+  return u;
+}
+
 template <typename T, bool EXACT>
 __device__ __forceinline__ void gu_update_one(const GlobalUpdateArgs<T>& a, int64_t idx, T d, bool& bad) {
   if (idx < a.n_params) {
     T w = a.w[idx], v = a.mode ? a.v[idx] : T(0);
-    UpdateArgs<T> u{};
+    UpdateArgs<T> u = gu_split_args<T>(a);
     u.mode = a.mode;
     u.lr = a.lr;
     u.momentum = a.momentum;
@@ -508,6 +520,7 @@ __device__ __forceinline__ void gu_update_one(const GlobalUpdateArgs<T>& a, int6
     sgd_one<T, EXACT>(w, v, d, u);
     a.w[idx] = w;
     if (a.mode) a.v[idx] = v;
+    store_split<T>(u, idx, &w, 1);
     bad |= !isfinite(w);
   } else if (idx == a.n_params && a.loss_out) {
     *a.loss_out = d;
@@ -520,7 +533,7 @@ __global__ void __launch_bounds__(256) global_update_kernel(const __grid_constan
   constexpr int V = Vec<T>::kN;
   const int64_t nvec = a.len / V;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  UpdateArgs<T> u{};
+  UpdateArgs<T> u = gu_split_args<T>(a);  // carries w_hi / w_lo for store_split
   u.mode = a.mode;
   u.lr = a.lr;
   u.momentum = a.momentum;
@@ -571,6 +584,7 @@ __global__ void __launch_bounds__(256) global_update_kernel(const __grid_constan
       }
       st16(a.w + i0, w);
       if (a.mode) st16(a.v + i0, v);
+      store_split<T>(u, i0, w.v, V);
     } else {
 #pragma unroll
       for (int q = 0; q < V; ++q) gu_update_one<T, EXACT>(a, i0 + q, r.v[q], bad);

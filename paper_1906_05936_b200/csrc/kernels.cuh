@@ -111,6 +111,8 @@ struct GlobalUpdateArgs {
   T lr = T(0), momentum = T(0), weight_decay = T(0);
   T* loss_out = nullptr;
   unsigned* bad = nullptr;
+  float* w_hi = nullptr;  // fp32 only, may be null: TF32 hi/lo split of the updated weights (bucket parameter 0),
+  float* w_lo = nullptr;  // for the GEMMs that read pre-split weights (LSGD_TC_WSPLIT=0)
 };
 template <typename T>
 void launch_global_update(const GlobalUpdateArgs<T>& a, bool exact, cudaStream_t st, LaunchCounter& lc);

@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <map>
 #include <tuple>
+#include <type_traits>
 #include <mutex>
 
 #include "engine.hpp"
@@ -344,6 +345,7 @@ class RankImpl final : public Rank {
       check_health();
       const int32_t* given = nullptr;
       if (host_idx) given = host_idx + q * (shard_only ? static_cast<int64_t>(B_) * workers_.size() : spec_.global_batch());
+      spill_losses_if_due();
       issue_one(t_next_, given, shard_only);
       ++t_next_;
     }
@@ -357,6 +359,7 @@ class RankImpl final : public Rank {
       check_health();
       rows_x_ = static_cast<const T*>(x_host) + q * per;
       rows_y_ = y_host + q * static_cast<int64_t>(B_) * static_cast<int64_t>(ws_.size());
+      spill_losses_if_due();
       issue_one(t_next_, nullptr, false);
       rows_x_ = nullptr;
       rows_y_ = nullptr;
@@ -392,14 +395,32 @@ class RankImpl final : public Rank {
   int64_t steps_issued() const override { return t_next_; }
   int64_t updates_applied() const override { return applied_; }
 
+  // The device loss ring holds kLossCap rounds. Every kLossCap/2 issued steps the applied rounds not yet saved are
+  // copied to host memory (one host sync per kLossCap/2 steps), so the ring never overwrites an unsaved round and
+  // history() returns every iteration's loss however long the run.
+  void spill_losses_if_due() {
+    if (t_next_ == 0 || t_next_ % (kLossCap / 2) != 0) return;
+    synchronize();
+    spill_losses();
+  }
+  void spill_losses() {
+    if (applied_ <= spilled_) return;
+    check<Error>(applied_ - spilled_ <= kLossCap, "loss history: unsaved rounds were overwritten");
+    std::vector<T> ring(static_cast<size_t>(kLossCap));
+    LSGD_CUDA(cudaMemcpy(ring.data(), ws_[0].loss_hist, sizeof(T) * kLossCap, cudaMemcpyDeviceToHost));
+    loss_saved_.resize(static_cast<size_t>(applied_));
+    for (int64_t u = spilled_; u < applied_; ++u)
+      loss_saved_[static_cast<size_t>(u)] = ring[static_cast<size_t>(u % kLossCap)];
+    spilled_ = applied_;
+  }
+
   void history(double* loss, double* lr, int64_t n) override {
     LSGD_CUDA(cudaSetDevice(dev_));
     synchronize();
+    spill_losses();
     n = std::min(n, applied_);
-    std::vector<T> tmp(static_cast<size_t>(kLossCap));
-    LSGD_CUDA(cudaMemcpy(tmp.data(), ws_[0].loss_hist, sizeof(T) * kLossCap, cudaMemcpyDeviceToHost));
     for (int64_t u = 0; u < n; ++u) {
-      if (loss) loss[u] = static_cast<double>(tmp[static_cast<size_t>(u % kLossCap)]);
+      if (loss) loss[u] = static_cast<double>(loss_saved_[static_cast<size_t>(u)]);
       if (lr) lr[u] = spec_.lr(u);
     }
   }
@@ -1181,6 +1202,12 @@ class RankImpl final : public Rank {
       ga.weight_decay = static_cast<T>(spec_.c.weight_decay);
       ga.loss_out = bk.loss ? w.loss_hist + (t % kLossCap) : nullptr;
       ga.bad = bad_dev_;
+      if constexpr (std::is_same_v<T, float>) {
+        if (use_tc_ && !w.tc.weights_split_in_smem) {  // the GEMMs read pre-split weights: refresh this slot's too
+          ga.w_hi = w.tc.w_hi + bk.pstart;
+          ga.w_lo = w.tc.w_lo + bk.pstart;
+        }
+      }
       DstList<T> remote = ga.push;
       const int n_remote = ga.n_push;
       const bool fan_dma = dma(8) && n_remote > 0;
@@ -1527,6 +1554,8 @@ class RankImpl final : public Rank {
   int* timed_out_dev_ = nullptr;
   unsigned* bad_dev_ = nullptr;
   int64_t t_next_ = 0, applied_ = 0;
+  int64_t spilled_ = 0;          // rounds [0, spilled_) of the loss history are in loss_saved_
+  std::vector<T> loss_saved_;
   int64_t t_cur_ = 0;  // step being issued (round counter of the producers' staged flags)
   T* hist_ = nullptr;
   LaunchCounter lc_;

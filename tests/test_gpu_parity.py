@@ -319,3 +319,15 @@ def test_phase_spans_and_io_overlaps_global_allreduce(n_devices, n_gpus, tmp_pat
     assert rows[0] == lsgd.K_METRICS_HEADER and len(rows) == 9
     io_s = np.array([float(x.split(",")[8]) for x in rows[1:]])
     assert np.all(io_s > 0.015)  # the injected 20 ms io delay shows up in t_io_s
+
+
+def test_loss_history_longer_than_the_device_ring():
+    """Runs past the 65,536-round device loss ring: history() still returns every iteration's loss (the ring is
+    spilled to host memory every 32,768 steps; ADVICE r1 found it silently wrapping)."""
+    kw = dict(algorithm="lsgd", n_workers=1, n_groups=1, layer_sizes=[8, 4], n_samples=256, n_features=8,
+              n_classes=4, spread=6.0, mode="plain", local_batch=4, seed=3)
+    long = lsgd.run_train(lsgd.TrainConfig(iterations=70_000, **kw))
+    short = lsgd.run_train(lsgd.TrainConfig(iterations=300, **kw))
+    assert long.loss_history.shape == (70_000,) and np.isfinite(long.loss_history).all()
+    assert np.array_equal(long.loss_history[:300], short.loss_history)  # same rounds, same bits (deterministic)
+    assert not np.array_equal(long.loss_history[65_536:65_836], long.loss_history[:300])  # not wrapped

@@ -33,8 +33,9 @@ def _cfg(dtype, n, groups):
     return cfg
 
 
-def _worker(rank, world, port, dtype, groups, mode, out):
+def _worker(rank, world, port, dtype, groups, mode, out, env=None):
     sys.path.insert(0, ROOT)
+    os.environ.update(env or {})  # before the library reads its knobs (first Rank)
     import torch
     import torch.distributed as dist
 
@@ -71,11 +72,11 @@ def _worker(rank, world, port, dtype, groups, mode, out):
         dist.destroy_process_group()
 
 
-def _spawn(world, dtype, groups, mode):
+def _spawn(world, dtype, groups, mode, env=None):
     import torch.multiprocessing as mp
     mgr = mp.get_context("spawn").Manager()  # no fork() of this multi-threaded process
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), dtype, groups, mode, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), dtype, groups, mode, out, env), nprocs=world, join=True)
     return dict(out)
 
 
@@ -105,3 +106,17 @@ def test_missing_peer_is_a_transport_error_not_a_hang(n_gpus):
         pytest.skip("needs 2 GPUs")
     out = _spawn(2, "fp64", 2, "timeout")
     assert out["err"] == "TransportError", out
+
+
+@pytest.mark.parametrize("groups,per_group", [(2, 1), (2, 2)])
+def test_hbm_weight_split_is_bitwise_the_smem_split_multi_gpu(groups, per_group, n_gpus):
+    """LSGD_TC_WSPLIT=0 (forward / dX GEMMs read the TF32 hi/lo weights the updates write to HBM) gives the same bits
+    as the default in-SMEM split at N > 1, where each owner updates its own slot inside the fused global kernel
+    (global_update_kernel must refresh w_hi / w_lo of that slot too)."""
+    n = groups * per_group
+    if n_gpus < n:
+        pytest.skip(f"needs {n} GPUs")
+    smem = _spawn(n, "fp32", groups, "train")
+    hbm = _spawn(n, "fp32", groups, "train", env={"LSGD_TC_WSPLIT": "0"})
+    for q in range(n):
+        assert np.array_equal(smem[q].view(np.uint64), hbm[q].view(np.uint64)), q
