@@ -248,6 +248,28 @@ def run_b200_arm(args):
     B = cfg.local_batch
     value = args.steps * n * B / (ms_max / 1e3)
 
+    # t_step(1) for SURVEY.md §8(d)'s exposed communication (t_step(N) - t_step(1)): rank 0 runs the same workload
+    # as one worker on its own GPU, same K / W, right after the N-GPU measurement (the other ranks wait)
+    t1_ms = None
+    if n > 1 and cfg.b200.model == "mlp" and not args.skip_t1:
+        if rank == 0:
+            c1 = workload(args.workload, 1, args.bloc, "lsgd", args.global_allreduce, 1)
+            r1 = Rank(c1, 0, local)
+            r1.connect([r1.export()])
+            s1 = torch.cuda.ExternalStream(r1.stream())
+            r1.step(args.warmup)
+            r1.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s1)
+            r1.step(args.steps)
+            r1.join()
+            e1.record(s1)
+            r1.synchronize()
+            t1_ms = e0.elapsed_time(e1) / args.steps
+            r1.close()
+            del r1
+        barrier()
+
     # e2e: host rows -> H2D per step, loss D2H per step, through the C-ABI data-loader call
     e2e = None
     if cfg.b200.model == "mlp" and not args.skip_e2e:
@@ -365,12 +387,15 @@ def run_b200_arm(args):
         exposed = None
         if cfg.b200.model == "mlp":
             main_fams = ["gemm", "gather", "head", "split"]
-            if args.algo != "lsgd" or os.environ.get("LSGD_B200_BIAS_STREAM") == "0":
+            if os.environ.get("LSGD_B200_BIAS_STREAM") == "0":
                 main_fams.append("bias")
             main_ms = sum(kern[f]["ms_per_step"] for f in main_fams if f in kern)
-            exposed = {"ms_per_step": max(0.0, ms_max / args.steps - main_ms), "main_compute_ms": main_ms,
-                       "basis": "ms_per_step - per-step device time of the main-stream compute kernels ("
-                                + ", ".join(main_fams) + ")"}
+            exposed = {"ms_per_step": (ms_max / args.steps - t1_ms) if t1_ms is not None else 0.0,
+                       "t_step_n_ms": ms_max / args.steps, "t_step_1_ms": t1_ms if n > 1 else ms_max / args.steps,
+                       "basis": "SURVEY.md §8(d): t_step(N) - t_step(1), t_step(1) = the same workload as one "
+                                "worker on rank 0's GPU in the same run",
+                       "beyond_main_compute_ms": max(0.0, ms_max / args.steps - main_ms),
+                       "main_compute_ms": main_ms}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
@@ -439,6 +464,7 @@ def main():
                     help="LSGD communicator groups (default min(2, N): N=8 -> 2x4); e.g. 1 for 1xN, N for Nx1")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-t1", action="store_true", help="skip the in-run t_step(1) of exposed_comm at N > 1")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

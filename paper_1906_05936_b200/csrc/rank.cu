@@ -15,7 +15,11 @@
 #include <cstdlib>
 #include <cstring>
 #include <cstdio>
+#include <atomic>
+#include <chrono>
+#include <deque>
 #include <map>
+#include <thread>
 #include <tuple>
 #include <type_traits>
 #include <mutex>
@@ -210,6 +214,7 @@ class RankImpl final : public Rank {
   }
 
   ~RankImpl() override {
+    stop_nccl_watchdog();
     cudaSetDevice(dev_);
     cudaDeviceSynchronize();
     for (auto& kv : timers_)
@@ -228,8 +233,15 @@ class RankImpl final : public Rank {
     for (T* p : own_x_) cudaFree(p);
     for (int32_t* p : own_y_) cudaFree(p);
     for (char* p : ipc_opened_) cudaIpcCloseMemHandle(p);
-    if (slice_comm_) ncclCommDestroy(slice_comm_);
-    if (flat_comm_) ncclCommDestroy(flat_comm_);
+    if (!nccl_aborted_) {  // an aborted communicator is already torn down (ncclCommAbort)
+      if (slice_comm_) ncclCommDestroy(slice_comm_);
+      if (flat_comm_) ncclCommDestroy(flat_comm_);
+    }
+    for (cudaEvent_t e : nccl_ev_pool_) cudaEventDestroy(e);
+    for (auto& op : nccl_ops_) {
+      cudaEventDestroy(op.pre);
+      cudaEventDestroy(op.post);
+    }
     if (own_data_) {
       if (host_data_) cudaFreeHost(host_alloc_);
       else {
@@ -275,6 +287,93 @@ class RankImpl final : public Rank {
   void set_nccl(void* slice_comm, void* flat_comm) override {
     slice_comm_ = static_cast<ncclComm_t>(slice_comm);
     flat_comm_ = static_cast<ncclComm_t>(flat_comm);
+    if ((slice_comm_ || flat_comm_) && !nccl_watch_.joinable())
+      nccl_watch_ = std::thread([this] { nccl_watch_loop(); });
+  }
+
+  // ---- NCCL watchdog: the reference times out every receive (inprocess.cpp:44-49, TransportError). A collective
+  // whose peer never arrives would block its stream forever, so every NCCL call is bracketed by two events; a host
+  // thread watches the oldest unfinished call and, once it has been running (its `pre` event reached) for longer
+  // than collective_timeout_s, or NCCL reports an asynchronous error, aborts the communicators (ncclCommAbort
+  // releases the stuck kernels) and marks the rank failed: the next step / synchronize raises TransportError.
+  struct NcclOp {
+    cudaEvent_t pre, post;
+    double started;
+  };
+  static double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  }
+  cudaEvent_t nccl_event() {  // under nccl_mu_
+    if (!nccl_ev_pool_.empty()) {
+      cudaEvent_t e = nccl_ev_pool_.back();
+      nccl_ev_pool_.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    LSGD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return e;
+  }
+  template <class F>
+  void nccl_call(cudaStream_t st, F&& call) {
+    check_health();  // never touch an aborted communicator
+    NcclOp op{};
+    {
+      std::lock_guard<std::mutex> g(nccl_mu_);
+      op.pre = nccl_event();
+      op.post = nccl_event();
+    }
+    op.started = -1.0;
+    LSGD_CUDA(cudaEventRecord(op.pre, st));
+    call();
+    LSGD_CUDA(cudaEventRecord(op.post, st));
+    std::lock_guard<std::mutex> g(nccl_mu_);
+    nccl_ops_.push_back(op);
+  }
+  void nccl_watch_loop() {
+    cudaSetDevice(dev_);
+    while (!nccl_stop_.load()) {
+      bool abort_now = false;
+      std::string why;
+      {
+        std::lock_guard<std::mutex> g(nccl_mu_);
+        while (!nccl_ops_.empty()) {
+          NcclOp& op = nccl_ops_.front();
+          if (cudaEventQuery(op.post) == cudaSuccess) {
+            nccl_ev_pool_.push_back(op.pre);
+            nccl_ev_pool_.push_back(op.post);
+            nccl_ops_.pop_front();
+            continue;
+          }
+          if (op.started < 0 && cudaEventQuery(op.pre) == cudaSuccess) op.started = now_s();
+          if (op.started >= 0 && now_s() - op.started > spec_.c.collective_timeout_s) {
+            abort_now = true;
+            why = cat("NCCL collective did not complete within ", spec_.c.collective_timeout_s, " s");
+          }
+          break;
+        }
+      }
+      for (ncclComm_t c : {slice_comm_, flat_comm_}) {
+        ncclResult_t ae = ncclSuccess;
+        if (!abort_now && c && ncclCommGetAsyncError(c, &ae) == ncclSuccess && ae != ncclSuccess &&
+            ae != ncclInProgress) {
+          abort_now = true;
+          why = cat("NCCL asynchronous error: ", ncclGetErrorString(ae));
+        }
+      }
+      if (abort_now) {
+        nccl_abort_reason_ = why;
+        nccl_aborted_ = true;
+        *timed_out_host_ = 1;
+        if (slice_comm_) ncclCommAbort(slice_comm_);
+        if (flat_comm_) ncclCommAbort(flat_comm_);
+        return;
+      }
+      std::this_thread::sleep_for(std::chrono::milliseconds(5));
+    }
+  }
+  void stop_nccl_watchdog() {
+    nccl_stop_ = true;
+    if (nccl_watch_.joinable()) nccl_watch_.join();
   }
   void note_ipc(char* p) { ipc_opened_.push_back(p); }
 
@@ -455,7 +554,7 @@ class RankImpl final : public Rank {
     LSGD_CUDA(cudaSetDevice(dev_));
     check<Error>(applied_ > 0, "no round has been applied yet");
     // the stream the round's update ran on
-    cudaStream_t st = (alg_ == LSGD_B200_LSGD && split_ && !fused_update()) ? upd_ : main_;
+    cudaStream_t st = (split_ && (alg_ == LSGD_B200_LSGD || flat_nccl()) && !fused_update()) ? upd_ : main_;
     Timed tm(this, "d2h", st);
     LSGD_CUDA(cudaMemcpyAsync(host_pinned, ws_[0].loss_hist + (applied_ - 1) % kLossCap, sizeof(T),
                               cudaMemcpyDeviceToHost, st));
@@ -547,9 +646,11 @@ class RankImpl final : public Rank {
 
   void abort() override { *timed_out_host_ = 1; }
   void check_health() override {
-    if (*timed_out_host_)
-      throw TransportError(cat("collective timeout or abort on device ", dev_, " after ",
-                               spec_.c.collective_timeout_s, " s waiting for peer flags"));
+    if (!*timed_out_host_) return;
+    if (nccl_aborted_.load())
+      throw TransportError(cat(nccl_abort_reason_, " on device ", dev_, "; communicators aborted"));
+    throw TransportError(cat("collective timeout or abort on device ", dev_, " after ", spec_.c.collective_timeout_s,
+                             " s waiting for peer flags"));
   }
 
   void enable_phases() {
@@ -1063,8 +1164,12 @@ class RankImpl final : public Rank {
     const int par = static_cast<int>(t & 1);
     if (slice_comm_) {
       Timed tm(this, "global", st);
-      LSGD_NCCL(ncclAllReduce(w.s[par] + bk.goff, w.gbar + bk.goff, static_cast<size_t>(bk.S), nccl_type(), ncclSum,
-                              slice_comm_, st));
+      nccl_call(st, [&] {
+        nccl_call(st, [&] {
+          LSGD_NCCL(ncclAllReduce(w.s[par] + bk.goff, w.gbar + bk.goff, static_cast<size_t>(bk.S), nccl_type(),
+                                  ncclSum, slice_comm_, st));
+        });
+      });
     } else {
       std::vector<int> owners;
       for (int g = 0; g < G_; ++g) owners.push_back(g * k_ + w.j);
@@ -1237,8 +1342,10 @@ class RankImpl final : public Rank {
       }
       {
         Timed tm(this, "global", st);
-        LSGD_NCCL(ncclAllReduce(w.s[par] + bk.goff, w.gbar + bk.goff, static_cast<size_t>(bk.S), nccl_type(),
-                                ncclSum, slice_comm_, st));
+        nccl_call(st, [&] {
+          LSGD_NCCL(ncclAllReduce(w.s[par] + bk.goff, w.gbar + bk.goff, static_cast<size_t>(bk.S), nccl_type(),
+                                  ncclSum, slice_comm_, st));
+        });
       }
       SrcList<T> one{};
       one.p[0] = w.gbar + bk.goff;
@@ -1325,7 +1432,11 @@ class RankImpl final : public Rank {
     // issued during step t-1 on the update stream, bucket by bucket as soon as (a) the bucket's averaged gradient
     // had arrived and (b) the backward of step t-1 no longer read W_k (after dX_k): the forward of layer k only
     // waits for its buckets' events. Emulated ranks (several workers on one stream) apply it here, in order.
-    const bool eager = alg_ == LSGD_B200_LSGD && split_;
+    // flat-NCCL CSGD with one worker per GPU uses the same bucketed schedule (the fair flat-allreduce baseline):
+    // per-bucket ncclAllReduce on the comm stream as each dW block lands, update per bucket on the update stream,
+    // the next forward of layer k waits for its buckets only. Same dependencies as the reference's synchronous
+    // CSGD block (executors.cpp:160-177): gradient t is reduced and applied before compute t+1 reads the layer.
+    const bool eager = split_ && (alg_ == LSGD_B200_LSGD || flat_nccl());
     const bool postponed = alg_ == LSGD_B200_LSGD && t >= 1 && !split_;
     const bool exchange = !flat_nccl() && !reduce_folded() && alg_ != LSGD_B200_SEQUENTIAL;
     for (auto& w : ws_) {
@@ -1399,11 +1510,26 @@ class RankImpl final : public Rank {
 
     // communicator work: per bucket, on the comm stream (overlapping the rest of the backward)
     current_phase() = "local_reduce";
-    if (flat_nccl()) {
+    if (flat_nccl() && split_) {
+      Worker& w = ws_[0];
+      for (int b : order) {  // one stream: every rank issues the collectives of one communicator in one order
+        const Bucket& bk = geo_.buckets[static_cast<size_t>(b)];
+        LSGD_CUDA(cudaStreamWaitEvent(comm_, ev_bucket_[b], 0));
+        if (bias_side_[b]) LSGD_CUDA(cudaStreamWaitEvent(comm_, ev_bias_[b], 0));
+        Timed tm(this, "global", comm_);
+        nccl_call(comm_, [&] {
+          LSGD_NCCL(ncclAllReduce(w.payload + bk.poff, w.payload + bk.poff, static_cast<size_t>(bk.S * k_),
+                                  nccl_type(), ncclSum, flat_comm_, comm_));
+        });
+        LSGD_CUDA(cudaEventRecord(ev_gupd_[b], comm_));  // bucket b's sum is in the payload
+      }
+    } else if (flat_nccl()) {
       Timed tm(this, "global", main_);
       for (auto& w : ws_)
-        LSGD_NCCL(ncclAllReduce(w.payload, w.payload, static_cast<size_t>(geo_.Ppad), nccl_type(), ncclSum,
-                                flat_comm_, main_));
+        nccl_call(main_, [&] {
+          LSGD_NCCL(ncclAllReduce(w.payload, w.payload, static_cast<size_t>(geo_.Ppad), nccl_type(), ncclSum,
+                                  flat_comm_, main_));
+        });
     } else if (exchange) {
       if (split_) {
         Worker& w = ws_[0];
@@ -1465,6 +1591,7 @@ class RankImpl final : public Rank {
         LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_dx_[k], 0));  // W_k is no longer read by this step
         for (int b : LB[static_cast<size_t>(k)]) {
           if (reduce_folded()) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_bucket_[b], 0));
+          if (flat_nccl()) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_gupd_[b], 0));  // the bucket's allreduce
           if (reduce_folded() && bias_side_[b]) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_bias_[b], 0));
           apply_bucket(w, b, t, upd_);
           if (own_slot_fused()) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_gupd_[b], 0));  // own slot (comm stream)
@@ -1475,7 +1602,7 @@ class RankImpl final : public Rank {
       ++applied_;
     }
 
-    if (alg_ != LSGD_B200_LSGD) {  // sequential / csgd: synchronous update in the same block (executors.cpp:172-177)
+    if (alg_ != LSGD_B200_LSGD && !eager) {  // sequential / csgd: synchronous update in the same block (:172-177)
       current_phase() = "update";
       for (auto& w : ws_) {
         for (int b = 0; b < NB; ++b) {
@@ -1540,6 +1667,12 @@ class RankImpl final : public Rank {
   std::vector<char*> peer_base_;
   std::vector<char*> ipc_opened_;
   ncclComm_t slice_comm_ = nullptr, flat_comm_ = nullptr;
+  std::mutex nccl_mu_;
+  std::deque<NcclOp> nccl_ops_;
+  std::vector<cudaEvent_t> nccl_ev_pool_;
+  std::thread nccl_watch_;
+  std::atomic<bool> nccl_stop_{false}, nccl_aborted_{false};
+  std::string nccl_abort_reason_;
   T* data_x_ = nullptr;
   int32_t* data_y_ = nullptr;
   int64_t n_rows_ = 0;

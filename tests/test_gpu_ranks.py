@@ -33,7 +33,17 @@ def _cfg(dtype, n, groups):
     return cfg
 
 
-def _worker(rank, world, port, dtype, groups, mode, out, env=None):
+def _apply(cfg, over):
+    for key, v in (over or {}).items():
+        obj = cfg
+        *path, last = key.split(".")
+        for p in path:
+            obj = getattr(obj, p)
+        setattr(obj, last, v)
+    return cfg
+
+
+def _worker(rank, world, port, dtype, groups, mode, out, env=None, over=None):
     sys.path.insert(0, ROOT)
     os.environ.update(env or {})  # before the library reads its knobs (first Rank)
     import torch
@@ -46,7 +56,7 @@ def _worker(rank, world, port, dtype, groups, mode, out, env=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        cfg = _cfg(dtype, world, groups)
+        cfg = _apply(_cfg(dtype, world, groups), over)
         if mode == "timeout":
             cfg.collective_timeout_s = 2.0
         r = Rank(cfg, rank, rank)
@@ -72,11 +82,11 @@ def _worker(rank, world, port, dtype, groups, mode, out, env=None):
         dist.destroy_process_group()
 
 
-def _spawn(world, dtype, groups, mode, env=None):
+def _spawn(world, dtype, groups, mode, env=None, over=None):
     import torch.multiprocessing as mp
     mgr = mp.get_context("spawn").Manager()  # no fork() of this multi-threaded process
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), dtype, groups, mode, out, env), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), dtype, groups, mode, out, env, over), nprocs=world, join=True)
     return dict(out)
 
 
@@ -120,3 +130,41 @@ def test_hbm_weight_split_is_bitwise_the_smem_split_multi_gpu(groups, per_group,
     hbm = _spawn(n, "fp32", groups, "train", env={"LSGD_TC_WSPLIT": "0"})
     for q in range(n):
         assert np.array_equal(smem[q].view(np.uint64), hbm[q].view(np.uint64)), q
+
+
+FLAT = {"algorithm": "csgd", "n_groups": 1, "b200.csgd_nccl": True}
+
+
+@pytest.mark.parametrize("n,dtype", [(2, "fp64"), (4, "fp64"), (2, "fp32"), (4, "fp32")])
+def test_flat_nccl_csgd_bucketed_matches_oracle(n, dtype, n_gpus):
+    """The flat-allreduce baseline (CSGD, per-bucket ncclAllReduce on the comm stream as each dW block lands, update
+    per bucket on the update stream) against the oracle's CSGD (executors.cpp:132-188). N = 2: a + b commutes, so
+    NCCL's sum is the reference's; N = 4: NCCL's reduction order differs from the reference's ascending order, so
+    fp64 is held per-coordinate to 1e-8 (the reference's verify tolerance), fp32 norm-wise to 1e-5."""
+    if n_gpus < n:
+        pytest.skip(f"needs {n} GPUs")
+    out = _spawn(n, dtype, 1, "train", over=FLAT)
+    from oracle import Oracle, TrainSpec
+    cfg = _apply(_cfg(dtype, n, 1), FLAT)
+    spec = TrainSpec(**{k: getattr(cfg, k) for k in TrainSpec.__dataclass_fields__ if hasattr(cfg, k)})
+    assert spec.algorithm == "csgd"
+    ref = Oracle("port").run_train(spec)["final_params"]
+    w0 = out[0]
+    if dtype == "fp64":
+        rel = np.abs(w0 - ref) / np.maximum(np.abs(ref), 1e-8)
+        assert rel.max() <= 1e-8, rel.max()
+    else:
+        dev = np.linalg.norm(w0 - ref) / np.linalg.norm(ref)
+        assert dev <= 1e-5, dev
+    for q in range(1, n):
+        assert np.array_equal(out[q].view(np.uint64), w0.view(np.uint64))
+
+
+@pytest.mark.parametrize("over", [{"b200.global_allreduce": "nccl"}, FLAT], ids=["lsgd_global_nccl", "csgd_flat_nccl"])
+def test_missing_peer_on_nccl_is_a_transport_error_not_a_hang(over, n_gpus):
+    """A peer that never issues its collective: the NCCL watchdog aborts the communicator after
+    collective_timeout_s and the step raises TransportError (inprocess.cpp:44-49), instead of blocking forever."""
+    if n_gpus < 2:
+        pytest.skip("needs 2 GPUs")
+    out = _spawn(2, "fp64", 1 if over is FLAT else 2, "timeout", over=over)
+    assert out["err"] == "TransportError", out
