@@ -183,3 +183,13 @@ def test_metrics_csv_schema_matches_the_reference(tmp_path):
     assert float(row[5]) == 1 * 10 / 100  # epoch = t * global_batch / n
     assert abs(float(row[11]) - 0.2) < 1e-12  # widest global allreduce span
     assert abs(float(row[8]) - 0.05) < 1e-12 and abs(float(row[14]) - 0.55) < 1e-12
+
+
+def test_library_exports_every_testing_symbol():
+    text = open(os.path.join(ROOT, "include", "lsgd_b200_testing.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    syms = sorted(set(re.findall(r"\b(lsgd_b200_test_[a-z0-9_]+)\s*\(", text)))
+    assert "lsgd_b200_test_exchange_kernel" in syms
+    lib = ctypes.CDLL(N.LIB_PATH)
+    for s in syms:
+        assert hasattr(lib, s), f"{s} declared in include/lsgd_b200_testing.h but not exported"
