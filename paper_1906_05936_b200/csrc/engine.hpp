@@ -129,6 +129,12 @@ struct TrainOutputs {
 };
 void run_world(const RunSpec& spec, bool want_history, bool want_workers, TrainOutputs& out);
 void enable_phase_recording(Rank* r);
+// Non-blocking NCCL communicators (ncclConfig_t.blocking = 0): every NCCL call returns at once and the host polls
+// ncclCommGetAsyncError with a deadline, so a peer that never joins an init or a collective surfaces as
+// TransportError (ncclCommAbort) instead of blocking the host thread (inprocess.cpp:44-49).
+// uid: the ncclUniqueId bytes. nccl_init_all: one communicator per device of `devs` from one thread (grouped).
+void* nccl_init_rank(int nranks, const void* uid, int rank, double timeout_s);
+std::vector<void*> nccl_init_all(const std::vector<int>& devs, double timeout_s);
 void note_ipc_mapping(Rank* r, char* p);
 
 // Parallel, bit-exact blob generator (SplitMix64 is a counter: draw k of Rng(s) = mix(s + (k+1)*gamma)).

@@ -37,6 +37,38 @@ constexpr int64_t kLossCap = 1 << 16;  // device loss history ring per rank
 
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
+double steady_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// Poll a non-blocking communicator until its pending call has been enqueued (ncclInProgress -> ncclSuccess). On
+// an error or past the deadline the communicator is aborted and TransportError raised. Returns normally on success.
+void nccl_settle(ncclComm_t c, double timeout_s, const char* what) {
+  const double t0 = steady_s();
+  for (;;) {
+    ncclResult_t ae = ncclSuccess;
+    ncclResult_t r = ncclCommGetAsyncError(c, &ae);
+    if (r != ncclSuccess) ae = r;
+    if (ae == ncclSuccess) return;
+    if (ae != ncclInProgress) {
+      ncclCommAbort(c);
+      throw TransportError(cat("NCCL ", what, " failed: ", ncclGetErrorString(ae), "; communicator aborted"));
+    }
+    if (steady_s() - t0 > timeout_s) {
+      ncclCommAbort(c);
+      throw TransportError(cat("NCCL ", what, " did not complete within ", timeout_s,
+                               " s (a peer never joined); communicator aborted"));
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
+ncclConfig_t nonblocking_config() {
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  cfg.blocking = 0;
+  return cfg;
+}
+
 struct PhaseEvents {
   cudaEvent_t ev[6][2];
   bool used[6];
@@ -300,9 +332,6 @@ class RankImpl final : public Rank {
     cudaEvent_t pre, post;
     double started;
   };
-  static double now_s() {
-    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
-  }
   cudaEvent_t nccl_event() {  // under nccl_mu_
     if (!nccl_ev_pool_.empty()) {
       cudaEvent_t e = nccl_ev_pool_.back();
@@ -313,8 +342,11 @@ class RankImpl final : public Rank {
     LSGD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     return e;
   }
+  // `call` issues one collective on `comm` and returns its ncclResult_t (ncclInProgress on a non-blocking
+  // communicator); the host then polls until it is enqueued (bounded: nccl_settle), and the watchdog thread takes
+  // over for the device side.
   template <class F>
-  void nccl_call(cudaStream_t st, F&& call) {
+  void nccl_call(cudaStream_t st, ncclComm_t comm, F&& call) {
     check_health();  // never touch an aborted communicator
     NcclOp op{};
     {
@@ -324,10 +356,52 @@ class RankImpl final : public Rank {
     }
     op.started = -1.0;
     LSGD_CUDA(cudaEventRecord(op.pre, st));
-    call();
+    ncclResult_t r;
+    {
+      std::lock_guard<std::mutex> g(nccl_api_mu_);
+      r = call();
+    }
+    if (r != ncclSuccess && r != ncclInProgress) {
+      mark_nccl_aborted(cat("NCCL error ", ncclGetErrorString(r)));
+      check_health();
+    }
+    try {
+      for (;;) {  // bounded host-side enqueue (lazy connection setup needs every peer)
+        ncclResult_t ae = ncclSuccess;
+        {
+          std::lock_guard<std::mutex> g(nccl_api_mu_);
+          ncclCommGetAsyncError(comm, &ae);
+        }
+        if (ae == ncclSuccess) break;
+        if (ae != ncclInProgress)
+          throw TransportError(cat("NCCL collective failed: ", ncclGetErrorString(ae)));
+        if (steady_s() - op_t0_or(op) > spec_.c.collective_timeout_s)
+          throw TransportError(cat("NCCL collective was not enqueued within ", spec_.c.collective_timeout_s,
+                                   " s (a peer never joined)"));
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
+      }
+    } catch (const TransportError& e) {
+      mark_nccl_aborted(e.what());
+      check_health();
+    }
     LSGD_CUDA(cudaEventRecord(op.post, st));
     std::lock_guard<std::mutex> g(nccl_mu_);
     nccl_ops_.push_back(op);
+  }
+  double op_t0_or(NcclOp& op) {
+    if (op.started < 0) op.started = steady_s();
+    return op.started;
+  }
+  // Abort every communicator of this rank (once) and fail the rank: the next step / synchronize raises
+  // TransportError with `why`.
+  void mark_nccl_aborted(const std::string& why) {
+    std::lock_guard<std::mutex> g(nccl_api_mu_);
+    if (nccl_aborted_.load()) return;
+    nccl_abort_reason_ = why;
+    nccl_aborted_ = true;
+    *timed_out_host_ = 1;
+    if (slice_comm_) ncclCommAbort(slice_comm_);
+    if (flat_comm_) ncclCommAbort(flat_comm_);
   }
   void nccl_watch_loop() {
     cudaSetDevice(dev_);
@@ -344,28 +418,16 @@ class RankImpl final : public Rank {
             nccl_ops_.pop_front();
             continue;
           }
-          if (op.started < 0 && cudaEventQuery(op.pre) == cudaSuccess) op.started = now_s();
-          if (op.started >= 0 && now_s() - op.started > spec_.c.collective_timeout_s) {
+          if (op.started < 0 && cudaEventQuery(op.pre) == cudaSuccess) op.started = steady_s();
+          if (op.started >= 0 && steady_s() - op.started > spec_.c.collective_timeout_s) {
             abort_now = true;
             why = cat("NCCL collective did not complete within ", spec_.c.collective_timeout_s, " s");
           }
           break;
         }
       }
-      for (ncclComm_t c : {slice_comm_, flat_comm_}) {
-        ncclResult_t ae = ncclSuccess;
-        if (!abort_now && c && ncclCommGetAsyncError(c, &ae) == ncclSuccess && ae != ncclSuccess &&
-            ae != ncclInProgress) {
-          abort_now = true;
-          why = cat("NCCL asynchronous error: ", ncclGetErrorString(ae));
-        }
-      }
       if (abort_now) {
-        nccl_abort_reason_ = why;
-        nccl_aborted_ = true;
-        *timed_out_host_ = 1;
-        if (slice_comm_) ncclCommAbort(slice_comm_);
-        if (flat_comm_) ncclCommAbort(flat_comm_);
+        mark_nccl_aborted(why);
         return;
       }
       std::this_thread::sleep_for(std::chrono::milliseconds(5));
@@ -1164,11 +1226,9 @@ class RankImpl final : public Rank {
     const int par = static_cast<int>(t & 1);
     if (slice_comm_) {
       Timed tm(this, "global", st);
-      nccl_call(st, [&] {
-        nccl_call(st, [&] {
-          LSGD_NCCL(ncclAllReduce(w.s[par] + bk.goff, w.gbar + bk.goff, static_cast<size_t>(bk.S), nccl_type(),
-                                  ncclSum, slice_comm_, st));
-        });
+      nccl_call(st, slice_comm_, [&] {
+        return ncclAllReduce(w.s[par] + bk.goff, w.gbar + bk.goff, static_cast<size_t>(bk.S), nccl_type(), ncclSum,
+                             slice_comm_, st);
       });
     } else {
       std::vector<int> owners;
@@ -1342,9 +1402,9 @@ class RankImpl final : public Rank {
       }
       {
         Timed tm(this, "global", st);
-        nccl_call(st, [&] {
-          LSGD_NCCL(ncclAllReduce(w.s[par] + bk.goff, w.gbar + bk.goff, static_cast<size_t>(bk.S), nccl_type(),
-                                  ncclSum, slice_comm_, st));
+        nccl_call(st, slice_comm_, [&] {
+          return ncclAllReduce(w.s[par] + bk.goff, w.gbar + bk.goff, static_cast<size_t>(bk.S), nccl_type(),
+                               ncclSum, slice_comm_, st);
         });
       }
       SrcList<T> one{};
@@ -1517,18 +1577,18 @@ class RankImpl final : public Rank {
         LSGD_CUDA(cudaStreamWaitEvent(comm_, ev_bucket_[b], 0));
         if (bias_side_[b]) LSGD_CUDA(cudaStreamWaitEvent(comm_, ev_bias_[b], 0));
         Timed tm(this, "global", comm_);
-        nccl_call(comm_, [&] {
-          LSGD_NCCL(ncclAllReduce(w.payload + bk.poff, w.payload + bk.poff, static_cast<size_t>(bk.S * k_),
-                                  nccl_type(), ncclSum, flat_comm_, comm_));
+        nccl_call(comm_, flat_comm_, [&] {
+          return ncclAllReduce(w.payload + bk.poff, w.payload + bk.poff, static_cast<size_t>(bk.S * k_), nccl_type(),
+                               ncclSum, flat_comm_, comm_);
         });
         LSGD_CUDA(cudaEventRecord(ev_gupd_[b], comm_));  // bucket b's sum is in the payload
       }
     } else if (flat_nccl()) {
       Timed tm(this, "global", main_);
       for (auto& w : ws_)
-        nccl_call(main_, [&] {
-          LSGD_NCCL(ncclAllReduce(w.payload, w.payload, static_cast<size_t>(geo_.Ppad), nccl_type(), ncclSum,
-                                  flat_comm_, main_));
+        nccl_call(main_, flat_comm_, [&] {
+          return ncclAllReduce(w.payload, w.payload, static_cast<size_t>(geo_.Ppad), nccl_type(), ncclSum,
+                               flat_comm_, main_);
         });
     } else if (exchange) {
       if (split_) {
@@ -1667,7 +1727,8 @@ class RankImpl final : public Rank {
   std::vector<char*> peer_base_;
   std::vector<char*> ipc_opened_;
   ncclComm_t slice_comm_ = nullptr, flat_comm_ = nullptr;
-  std::mutex nccl_mu_;
+  std::mutex nccl_mu_;      // nccl_ops_ / nccl_ev_pool_
+  std::mutex nccl_api_mu_;  // NCCL API calls of this rank's communicators (main thread vs watchdog)
   std::deque<NcclOp> nccl_ops_;
   std::vector<cudaEvent_t> nccl_ev_pool_;
   std::thread nccl_watch_;
@@ -1708,6 +1769,41 @@ std::unique_ptr<Rank> make_rank(const RunSpec& spec, int device, std::vector<int
 void enable_phase_recording(Rank* r) {
   if (auto* a = dynamic_cast<RankImpl<float>*>(r)) a->enable_phases();
   if (auto* b = dynamic_cast<RankImpl<double>*>(r)) b->enable_phases();
+}
+
+void* nccl_init_rank(int nranks, const void* uid, int rank, double timeout_s) {
+  ncclUniqueId id;
+  std::memcpy(&id, uid, sizeof(id));
+  ncclConfig_t cfg = nonblocking_config();
+  ncclComm_t c = nullptr;
+  ncclResult_t r = ncclCommInitRankConfig(&c, nranks, id, rank, &cfg);
+  if (r != ncclSuccess && r != ncclInProgress)
+    throw TransportError(cat("NCCL init failed: ", ncclGetErrorString(r)));
+  nccl_settle(c, timeout_s, "communicator init");
+  return c;
+}
+
+std::vector<void*> nccl_init_all(const std::vector<int>& devs, double timeout_s) {
+  ncclUniqueId id;
+  LSGD_NCCL(ncclGetUniqueId(&id));
+  const int n = static_cast<int>(devs.size());
+  std::vector<ncclComm_t> cs(static_cast<size_t>(n), nullptr);
+  ncclConfig_t cfg = nonblocking_config();
+  LSGD_NCCL(ncclGroupStart());
+  for (int i = 0; i < n; ++i) {
+    LSGD_CUDA(cudaSetDevice(devs[static_cast<size_t>(i)]));
+    ncclResult_t r = ncclCommInitRankConfig(&cs[static_cast<size_t>(i)], n, id, i, &cfg);
+    if (r != ncclSuccess && r != ncclInProgress)
+      throw TransportError(cat("NCCL init failed: ", ncclGetErrorString(r)));
+  }
+  ncclResult_t ge = ncclGroupEnd();
+  if (ge != ncclSuccess && ge != ncclInProgress) throw TransportError(cat("NCCL init failed: ", ncclGetErrorString(ge)));
+  std::vector<void*> out;
+  for (ncclComm_t c : cs) {
+    nccl_settle(c, timeout_s, "communicator init");
+    out.push_back(c);
+  }
+  return out;
 }
 
 void note_ipc_mapping(Rank* r, char* p) {

@@ -106,22 +106,19 @@ void run_world(const RunSpec& spec, bool want_history, bool want_workers, TrainO
       for (int w : q->workers()) r->set_peer_base(w, q->peer_block(w));
 
   // NCCL only when every rank hosts a single worker (one NCCL rank per device).
-  std::vector<ncclComm_t> comms_to_free;
   const bool one_each = ndev == N;
   if (one_each && spec.c.algorithm == LSGD_B200_LSGD && G > 1 && spec.c.global_algo == LSGD_B200_GLOBAL_NCCL) {
     for (int j = 0; j < k; ++j) {
       std::vector<int> devs;
       for (int g = 0; g < G; ++g) devs.push_back(g * k + j);
-      std::vector<ncclComm_t> cs(static_cast<size_t>(G));
-      LSGD_NCCL(ncclCommInitAll(cs.data(), G, devs.data()));
+      std::vector<void*> cs = nccl_init_all(devs, spec.c.collective_timeout_s);
       for (int g = 0; g < G; ++g) ranks[static_cast<size_t>(g * k + j)]->set_nccl(cs[static_cast<size_t>(g)], nullptr);
     }
   }
   if (one_each && spec.c.algorithm == LSGD_B200_CSGD && spec.c.csgd_nccl && N > 1) {
     std::vector<int> devs;
     for (int i = 0; i < N; ++i) devs.push_back(i);
-    std::vector<ncclComm_t> cs(static_cast<size_t>(N));
-    LSGD_NCCL(ncclCommInitAll(cs.data(), N, devs.data()));
+    std::vector<void*> cs = nccl_init_all(devs, spec.c.collective_timeout_s);
     for (int i = 0; i < N; ++i) ranks[static_cast<size_t>(i)]->set_nccl(nullptr, cs[static_cast<size_t>(i)]);
   }
 

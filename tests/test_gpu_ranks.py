@@ -75,6 +75,7 @@ def _worker(rank, world, port, dtype, groups, mode, out, env=None, over=None):
                 out["err"] = None
             except lsgd.LsgdError as e:
                 out["err"] = type(e).__name__
+                out["msg"] = str(e)
         dist.barrier()
         r.close()
         dist.barrier()
