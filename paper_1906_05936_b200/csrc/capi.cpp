@@ -278,12 +278,12 @@ int lsgd_b200_rank_connect(lsgd_b200_rank* r, const void* all_blobs) {
       const int j = r->id % k, g = r->id / k;
       ncclUniqueId uid;
       std::memcpy(&uid, all + j * kBlobBytes + kIpcBytes, kUidBytes);
-      slice = static_cast<ncclComm_t>(nccl_init_rank(G, &uid, g, s.c.collective_timeout_s));
+      slice = static_cast<ncclComm_t>(nccl_init_rank(G, &uid, g, init_timeout(s.c.collective_timeout_s)));
     }
     if (s.c.algorithm == LSGD_B200_CSGD && s.c.csgd_nccl && N > 1) {
       ncclUniqueId uid;
       std::memcpy(&uid, all + kIpcBytes + kUidBytes, kUidBytes);
-      flat = static_cast<ncclComm_t>(nccl_init_rank(N, &uid, r->id, s.c.collective_timeout_s));
+      flat = static_cast<ncclComm_t>(nccl_init_rank(N, &uid, r->id, init_timeout(s.c.collective_timeout_s)));
     }
     r->rank->set_nccl(slice, flat);
     enable_phase_recording(r->rank.get());

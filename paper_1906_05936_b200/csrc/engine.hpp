@@ -134,6 +134,9 @@ void enable_phase_recording(Rank* r);
 // TransportError (ncclCommAbort) instead of blocking the host thread (inprocess.cpp:44-49).
 // uid: the ncclUniqueId bytes. nccl_init_all: one communicator per device of `devs` from one thread (grouped).
 void* nccl_init_rank(int nranks, const void* uid, int rank, double timeout_s);
+// communicator setup (bootstrap, topology, channel connections) takes seconds: at least a minute, never less than
+// the collective timeout
+inline double init_timeout(double collective_timeout_s) { return collective_timeout_s > 60.0 ? collective_timeout_s : 60.0; }
 std::vector<void*> nccl_init_all(const std::vector<int>& devs, double timeout_s);
 void note_ipc_mapping(Rank* r, char* p);
 

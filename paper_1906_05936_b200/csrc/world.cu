@@ -111,14 +111,14 @@ void run_world(const RunSpec& spec, bool want_history, bool want_workers, TrainO
     for (int j = 0; j < k; ++j) {
       std::vector<int> devs;
       for (int g = 0; g < G; ++g) devs.push_back(g * k + j);
-      std::vector<void*> cs = nccl_init_all(devs, spec.c.collective_timeout_s);
+      std::vector<void*> cs = nccl_init_all(devs, init_timeout(spec.c.collective_timeout_s));
       for (int g = 0; g < G; ++g) ranks[static_cast<size_t>(g * k + j)]->set_nccl(cs[static_cast<size_t>(g)], nullptr);
     }
   }
   if (one_each && spec.c.algorithm == LSGD_B200_CSGD && spec.c.csgd_nccl && N > 1) {
     std::vector<int> devs;
     for (int i = 0; i < N; ++i) devs.push_back(i);
-    std::vector<void*> cs = nccl_init_all(devs, spec.c.collective_timeout_s);
+    std::vector<void*> cs = nccl_init_all(devs, init_timeout(spec.c.collective_timeout_s));
     for (int i = 0; i < N; ++i) ranks[static_cast<size_t>(i)]->set_nccl(nullptr, cs[static_cast<size_t>(i)]);
   }
 
