@@ -277,8 +277,8 @@ def run_b200_arm(args):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     nvl = NvlinkCounter(local) if n > 1 else None
     r.synchronize()
+    nvl0 = nvl.read() if nvl else None  # before the barrier: no rank may start its timed steps late
     barrier()
-    nvl0 = nvl.read() if nvl else None
     ev0.record(stream)
     r.step(args.steps)
     r.join()  # the last step's update / exchange streams finish inside the timed region
