@@ -652,23 +652,27 @@ class RankImpl final : public Rank {
           cudaEventDestroy(pr.second);
         }
       timers_.clear();
+      timer_tags_.clear();
     }
   }
   std::string timeline() override {
     synchronize();
-    std::vector<std::tuple<float, float, std::string>> rows;
-    for (auto& kv : timers_)
-      for (auto& pr : kv.second) {
+    std::vector<std::tuple<float, float, std::string, int>> rows;
+    for (auto& kv : timers_) {
+      const auto& tags = timer_tags_[kv.first];
+      for (size_t i = 0; i < kv.second.size(); ++i) {
         float a = 0, b = 0;
-        LSGD_CUDA(cudaEventElapsedTime(&a, base_ev_, pr.first));
-        LSGD_CUDA(cudaEventElapsedTime(&b, base_ev_, pr.second));
-        rows.emplace_back(a, b, kv.first);
+        LSGD_CUDA(cudaEventElapsedTime(&a, base_ev_, kv.second[i].first));
+        LSGD_CUDA(cudaEventElapsedTime(&b, base_ev_, kv.second[i].second));
+        rows.emplace_back(a, b, kv.first, i < tags.size() ? tags[i] : -1);
       }
+    }
     std::sort(rows.begin(), rows.end());
     std::string out;
-    char line[128];
-    for (auto& r : rows) {
-      std::snprintf(line, sizeof(line), "%s\t%.4f\t%.4f\n", std::get<2>(r).c_str(), std::get<0>(r), std::get<1>(r));
+    char line[160];
+    for (auto& r : rows) {  // family, start, end, tag (bucket id; 100 + k for layer-k GEMMs; -1 none)
+      std::snprintf(line, sizeof(line), "%s\t%.4f\t%.4f\t%d\n", std::get<2>(r).c_str(), std::get<0>(r),
+                    std::get<1>(r), std::get<3>(r));
       out += line;
     }
     return out;
@@ -891,6 +895,7 @@ class RankImpl final : public Rank {
         cudaEventCreate(&e);
         cudaEventRecord(e, st);
         r->timers_[fam].emplace_back(b, e);
+        r->timer_tags_[fam].push_back(r->tag_);
       }
     }
   };
@@ -993,6 +998,7 @@ class RankImpl final : public Rank {
   T* delta_buf(Worker& w, int k) { return w.dl[static_cast<size_t>(k)]; }
 
   void forward_layer(Worker& w, int k) {
+    tag_ = 100 + k;
     if (synth_) return;
     if (use_tc_) {
       if (k == 0 && !w.x_split_ready) {
@@ -1109,6 +1115,7 @@ class RankImpl final : public Rank {
 
   // Weight gradient of bucket b (a row block of dW_k, plus db_k for the layer's last block).
   void backward_bucket(Worker& w, int b) {
+    tag_ = b;
     const Bucket& bk0 = geo_.buckets[static_cast<size_t>(b)];
     if (bk0.blk_rows == 0) return;  // inside a block: its first bucket's GEMM wrote it
     Bucket bk = bk0;                  // the whole block: rows, and the bias when it ends the layer
@@ -1172,6 +1179,7 @@ class RankImpl final : public Rank {
 
   // Input gradient of layer k (masked delta of layer k-1); layer 0 has none (mlp.cpp:116).
   void backward_input(Worker& w, int k) {
+    tag_ = 200 + k;
     if (k == 0) return;
     Timed tm(this, "gemm", main_);
     if (use_tc_) {
@@ -1267,6 +1275,7 @@ class RankImpl final : public Rank {
     if (n) launch_wait_flags(fl, n, target, timeout_ns(), timed_out_dev_, st, lc_);
   }
   void exchange_push_bucket(Worker& w, int b, int64_t t, cudaStream_t st) {
+    tag_ = b;
     const Bucket& bk = geo_.buckets[static_cast<size_t>(b)];
     const int par = static_cast<int>(t & 1);
     const unsigned long long round = static_cast<unsigned long long>(t + 1);
@@ -1418,6 +1427,7 @@ class RankImpl final : public Rank {
   // K8 for bucket b of round u (executors.cpp:210-229): pull the k averaged sub-slices of the group, apply
   // sgd_update to the bucket's parameters, check finiteness, record the loss (last bucket).
   void apply_bucket(Worker& w, int b, int64_t u, cudaStream_t st) {
+    tag_ = b;
     const Bucket& bk = geo_.buckets[static_cast<size_t>(b)];
     const size_t wi = widx(w);
     if (b == 0) phase_mark(wi, u, 4, 0, st);
@@ -1755,6 +1765,8 @@ class RankImpl final : public Rank {
   LaunchCounter lc_;
   bool timing_ = false;
   std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> timers_;
+  std::map<std::string, std::vector<int>> timer_tags_;
+  int tag_ = -1;  // bucket (or 100 + layer) the launches being issued belong to (timeline only)
   cudaEvent_t t0_ev_ = nullptr;
   std::vector<std::vector<PhaseEvents>> phase_ev_;
 };

@@ -7,7 +7,7 @@ Run in the build container (needs /root/reference; builds oracle/_ref/liblsgd_re
 
 Runs the reference's own ``run_train`` (proj/src/executors.cpp:481-521) on the wide MLP 4096-8192-8192-512
 (P = 104,874,496), ``generate_synthetic(42, 65536, 4096, 512, 10.0)``, momentum SGD, B_loc = 512 on one worker
-(LSGD 1x1 = the bench's N=1 layout), T iterations in fp64, and writes ``cfg3_ref.npz``:
+(sequential = LSGD 1x1, the bench's N=1 layout), T iterations in fp64, and writes ``cfg3_ref.npz``:
 
   * ``idx``         - seeded sample of parameter coordinates: 16,384 from each weight matrix + every bias;
   * ``w{t}``        - the reference's w_t at those coordinates, t = 0..T;
@@ -38,7 +38,10 @@ PER_MATRIX = 16384
 
 
 def spec(iterations: int = T) -> TrainSpec:
-    return TrainSpec(algorithm="lsgd", n_workers=1, n_groups=1, layer_sizes=LAYERS, n_samples=65536,
+    # algorithm "sequential": the reference's LSGD 1x1 is bitwise the sequential run (ref_fixtures.json hashes
+    # seq = lsgd_1x1), and the sequential executor has no transport whose 30 s receive timeout a minutes-long
+    # cfg3 gradient would trip
+    return TrainSpec(algorithm="sequential", n_workers=1, n_groups=1, layer_sizes=LAYERS, n_samples=65536,
                      n_features=LAYERS[0], n_classes=LAYERS[-1], spread=10.0, mode="momentum",
                      local_batch=512, iterations=iterations, seed=42)
 

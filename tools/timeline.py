@@ -44,6 +44,9 @@ def main():
 
     cfg = bench.workload(args.workload, world, None, args.algo, args.global_allreduce)
     r = Rank(cfg, rank, local)
+    if rank == 0:
+        print("# buckets (id: layer rows n):", ", ".join(f"{i}: L{b[0]} {b[1]} {b[2]}" for i, b in enumerate(r.buckets()))
+              if hasattr(r, "buckets") else "")
     r.connect(allgather(r.export()))
     if args.rows:
         B, d = cfg.local_batch, cfg.n_features
@@ -75,10 +78,10 @@ def main():
     lines = [ln.split("\t") for ln in buf.value.decode().strip().splitlines()]
     if rank == 0:
         tot = {}
-        for fam, a, b in lines:
+        for fam, a, b, tag in lines:  # tag: bucket id, 100 + k forward / 200 + k dX GEMM of layer k
             tot[fam] = tot.get(fam, 0.0) + float(b) - float(a)
-            print(f"{fam:10s} {float(a):9.3f} {float(b):9.3f} {1e3 * (float(b) - float(a)):8.1f} us")
-        end = max(float(b) for _, _, b in lines)
+            print(f"{fam:10s} {tag:>4s} {float(a):9.3f} {float(b):9.3f} {1e3 * (float(b) - float(a)):8.1f} us")
+        end = max(float(b) for _, b in ((ln[1], ln[2]) for ln in lines))
         print(f"# {args.steps} steps span {end:.3f} ms ({end / args.steps:.3f} ms/step); busy ms per family: "
               + ", ".join(f"{k}={v / args.steps:.3f}" for k, v in sorted(tot.items())))
     r.close()
