@@ -117,51 +117,6 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-class NvlinkCounter:
-    """NVLink data bytes this GPU sent / received, from NVML's per-link throughput counters
-    (NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX, KiB, summed over the links), read before and after the timed region:
-    the achieved NVLink GB/s of the whole step, all exchange kernels and copy engines together."""
-
-    def __init__(self, gpu: int):
-        self.h = None
-        try:
-            import pynvml
-
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu)
-            self.links = [l for l in range(18) if self._link_up(l)]
-        except Exception:
-            self.h = None
-
-    def _link_up(self, l):
-        try:
-            return self.nv.nvmlDeviceGetNvLinkState(self.h, l) == 1
-        except Exception:
-            return False
-
-    def read(self):
-        if self.h is None or not self.links:
-            return None
-        ids = []
-        for l in self.links:
-            ids += [(self.nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, l), (self.nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, l)]
-        try:
-            vals = self.nv.nvmlDeviceGetFieldValues(self.h, ids)
-        except Exception:
-            return None
-        tx = rx = 0
-        for i, v in enumerate(vals):
-            if v.nvmlReturn != 0:
-                return None
-            x = v.value.ullVal * 1024  # KiB
-            if i % 2 == 0:
-                tx += x
-            else:
-                rx += x
-        return tx, rx
-
-
 def measured_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -275,29 +230,24 @@ def run_b200_arm(args):
         clocks.start()
     l0 = r.launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    nvl = NvlinkCounter(local) if n > 1 else None
     r.synchronize()
-    nvl0 = nvl.read() if nvl else None  # before the barrier: no rank may start its timed steps late
     barrier()
     ev0.record(stream)
     r.step(args.steps)
     r.join()  # the last step's update / exchange streams finish inside the timed region
     ev1.record(stream)
     r.synchronize()
-    nvl1 = nvl.read() if nvl else None
     ms = ev0.elapsed_time(ev1)
     nvlink = None
-    if nvl0 and nvl1:
-        tx, rx = nvl1[0] - nvl0[0], nvl1[1] - nvl0[1]
-        nvlink = {"tx_bytes_per_step": tx / args.steps, "rx_bytes_per_step": rx / args.steps,
-                  "tx_gbs": tx / (ms / 1e3) / 1e9, "rx_gbs": rx / (ms / 1e3) / 1e9, "links": len(nvl.links),
-                  "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX of rank 0's GPU over the timed region"}
+    if n > 1:
         G_, k_ = cfg.n_groups, n // cfg.n_groups
         # algorithmic egress per GPU and step: scatter (k-1)S + group-sum push (G-1)S + average fan-out (k-1)S with
-        # S = 4(P+1)/k (push exchange); flat allreduce 2(N-1)/N * 4(P+1)
-        algo_tx = (4.0 * (cfg.n_params + 1) * (2 * k_ + G_ - 3) / k_ if args.algo == "lsgd"
-                   else 2.0 * (n - 1) / n * 4.0 * (cfg.n_params + 1))
-        nvlink["algorithmic_tx_bytes_per_step"] = algo_tx
+        # S = 4(P+1)/k (push exchange); flat allreduce 2(N-1)/N * 4(P+1). Achieved = over the step time (the
+        # exchange overlaps the GEMMs); the kernels alone: profiles/r2_ncu_exchange_kernels.json
+        tx = (4.0 * (cfg.n_params + 1) * (2 * k_ + G_ - 3) / k_ if args.algo == "lsgd"
+              else 2.0 * (n - 1) / n * 4.0 * (cfg.n_params + 1))
+        nvlink = {"algorithmic_tx_bytes_per_step": tx, "tx_gbs_over_step": tx / (ms / args.steps / 1e3) / 1e9,
+                  "peak_gbs": 770.0, "peak_source": "B200_PROFILING.md measured peer copy per direction"}
     launches = r.launches() - l0
     clk = clocks.finish() if clocks else None
     r.timing(False)
