@@ -271,3 +271,51 @@ def test_full_size_cfg3_steps_match_torch_fp64():
         print(f"cfg3 step {t}: norm-wise deviation from float64 {devs}", flush=True)
         assert devs["tcgen05"] <= 1e-3 and devs["simt"] <= 1e-3, (t, devs)
         assert devs["tcgen05"] <= 1.6 * max(devs["simt"], 1e-6), (t, devs)
+
+
+def test_cfg3_steps_match_reference_fixtures():
+    """The bench configuration (BASELINE cfg3: MLP 4096-8192-8192-512, 105M parameters, 65,536 blobs, B_loc = 512,
+    momentum, one worker) on the production fp32 path, against the UNMODIFIED reference's own run_train in fp64
+    (tests/golden/cfg3_ref.npz from tests/golden/make_cfg3_golden.py; executors.cpp:481-521, mlp.cpp:238-273):
+      * w_0 is the reference's init rounded to fp32, bit for bit, at every sampled coordinate;
+      * after each of the T = 2 steps: ||w_t - w_t^ref|| / ||w_t^ref|| over 66,048 sampled coordinates (16,384 per
+        weight matrix + every bias) <= 3e-5 (t = 1) and <= 6e-5 (t = 2), the global and per-layer norms of w_t within
+        the same relative bounds, and the accumulated update w_t - w_0 within 2e-3 of the reference's (relative);
+      * the per-iteration losses within 1e-5 relative.
+    Why not 1e-5 on w after 100 steps here: at this width fp32 arithmetic itself drifts from float64 by ~1e-5 of
+    ||w|| per step and the dynamics amplify it (plain fp32 SIMT: 8.3e-6, 2.6e-5, 7.8e-5 after steps 1-3,
+    profiles/r1_fullsize_fp64.log); the 1e-5-after-100-steps contract holds at the reference's configs
+    (test_tc_training_matches_oracle_normwise, tests/test_gpu_parity.py)."""
+    ref = np.load(os.path.join(ROOT, "tests", "golden", "cfg3_ref.npz"))
+    T = int(ref["steps"])
+    layers = [4096, 8192, 8192, 512]
+    cfg = lsgd.TrainConfig(algorithm="lsgd", n_workers=1, n_groups=1, layer_sizes=layers, n_samples=65536,
+                           n_features=4096, n_classes=512, spread=10.0, mode="momentum", local_batch=512,
+                           iterations=T, record_history=True, seed=42)
+    cfg.b200.n_devices = 1
+    cfg.b200.gemm = "tcgen05"
+    r = lsgd.run_train(cfg)
+    h = r.param_history
+    idx = ref["idx"]
+    assert np.array_equal(h[0][idx], ref["w0"].astype(np.float32).astype(np.float64))
+    bounds = {1: 3e-5, 2: 6e-5}
+    offs, off = [], 0
+    for k in range(3):
+        nw = layers[k] * layers[k + 1]
+        offs.append((off, off + nw, off + nw, off + nw + layers[k + 1]))
+        off += nw + layers[k + 1]
+    report = {}
+    for t in range(1, T + 1):
+        w, wr = h[t][idx], ref[f"w{t}"]
+        dev = np.linalg.norm(w - wr) / np.linalg.norm(wr)
+        dnorm = abs(np.linalg.norm(h[t]) - float(ref[f"norm{t}"])) / float(ref[f"norm{t}"])
+        lnorm = np.array([[np.linalg.norm(h[t][a:b]), np.linalg.norm(h[t][c:d])] for a, b, c, d in offs])
+        ldev = np.abs(lnorm - ref[f"lnorm{t}"]) / ref[f"lnorm{t}"]
+        upd = np.linalg.norm((w - h[0][idx]) - (wr - ref["w0"])) / np.linalg.norm(wr - ref["w0"])
+        report[t] = (dev, dnorm, ldev.max(), upd)
+        assert dev <= bounds[t], report
+        assert dnorm <= bounds[t] and ldev.max() <= bounds[t], report
+        assert upd <= 2e-3, report
+    lrel = np.abs(r.loss_history - ref["loss"]) / np.abs(ref["loss"])
+    assert lrel.max() <= 1e-5, (lrel, report)
+    print("cfg3 vs reference (sampled dev, norm dev, layer-norm dev, update dev):", report, "loss", lrel)
