@@ -350,12 +350,21 @@ def run_b200_arm(args):
                     break
                 except (OSError, ValueError, KeyError):
                     pass
+            tf32 = None
+            try:  # measured dense TF32 peak on a B200 of this pool (tools/tf32_peak.py)
+                tf32 = json.load(open(os.path.join(ROOT, "profiles", "r2_tf32_peak.json")))["tf32_tflops_sustained"]
+            except (OSError, ValueError, KeyError):
+                pass
             roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                     "frac": (ach / peak) if ach else None, "traffic": traffic, "traffic_source": tsrc,
                     "traffic_unit": "bytes DRAM read+write per launch (= one step's GEMM sequence)",
                     "kernel": "forward+backward GEMM sequence per step (B_loc*F flops / its device time)",
                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (3xTF32 ceiling = peak/6)",
                     "frac_of_3xtf32_ceiling": (ach / (peak / 6)) if ach else None,
+                    "tf32_tflops_measured": tf32,
+                    "frac_of_measured_split_tf32_ceiling": (ach / (tf32 / 3)) if (ach and tf32) else None,
+                    "split_tf32_note": "each fp32 product = 3 TF32 MMAs (hi*hi + hi*lo + lo*hi): ceiling = TF32 / 3; "
+                                       "TF32 measured with cuBLAS (profiles/r2_tf32_peak.json)",
                     "flops_per_launch": B * F, "launches_timed": gemm_n}
         else:
             # synthetic gradient: the step is exchange + update; the roofline kernel is the update pass. With an
