@@ -41,6 +41,10 @@ int lsgd_b200_test_rank_timeline(lsgd_b200_rank* r, char* buf, int64_t cap);
 int lsgd_b200_test_exchange_kernel(int32_t kind, int32_t n_dev, int32_t k, int64_t len, int32_t reps, double* avg_ms,
                                    double* bytes_nvlink, double* bytes_local);
 
+/* The cross-GPU flag protocol check (wait_flags_kernel) on device 0: one flag holding `value`, waited for `target`
+ * with `max_lead`. *code = 0 passed, 2 protocol violation (value > target + max_lead), 1 timed out (50 ms). */
+int lsgd_b200_test_wait_flag(uint64_t value, uint64_t target, uint64_t max_lead, int32_t* code);
+
 #ifdef __cplusplus
 }
 #endif

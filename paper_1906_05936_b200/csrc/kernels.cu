@@ -371,15 +371,25 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-__global__ void wait_flags_kernel(FlagList fl, int n, unsigned long long target, unsigned long long timeout_ns,
-                                  volatile int* timed_out) {
+// Spin (one thread per flag) until every flag reaches `target`. Protocol check: a flag above target + max_lead
+// means its producer has already written a LATER round into a buffer this consumer has not read yet (a WAR
+// violation of the round-counter protocol); that is reported as code 2 through `timed_out` (TransportError on the
+// host) instead of silently consuming overwritten data.
+__global__ void wait_flags_kernel(FlagList fl, int n, unsigned long long target, unsigned long long max_lead,
+                                  unsigned long long timeout_ns, volatile int* timed_out) {
   const int i = threadIdx.x;
   if (i < n) {
     const unsigned long long t0 = globaltimer();
     for (;;) {
       unsigned long long v;
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(fl.f[i]) : "memory");
-      if (v >= target) break;
+      if (v >= target) {
+        if (v > target + max_lead) {
+          *timed_out = 2;
+          __threadfence_system();
+        }
+        break;
+      }
       if (*timed_out) break;  // another waiter (or the host, to abort) already gave up
       if (globaltimer() - t0 > timeout_ns) {
         *timed_out = 1;
@@ -723,8 +733,8 @@ void launch_update(const UpdateArgs<T>& a_in, bool exact, cudaStream_t st, Launc
 }
 
 void launch_wait_flags(FlagList flags, int n, unsigned long long target, unsigned long long timeout_ns,
-                       volatile int* timed_out, cudaStream_t st, LaunchCounter& lc) {
-  wait_flags_kernel<<<1, 32, 0, st>>>(flags, n, target, timeout_ns, timed_out);
+                       volatile int* timed_out, cudaStream_t st, LaunchCounter& lc, unsigned long long max_lead) {
+  wait_flags_kernel<<<1, 32, 0, st>>>(flags, n, target, max_lead, timeout_ns, timed_out);
   ++lc.n;
   LSGD_CUDA(cudaGetLastError());
 }

@@ -135,8 +135,10 @@ struct FlagList {
   const volatile unsigned long long* f[kMaxPeers];
 };
 // Spin (one CTA) until every flag >= target; on timeout writes 1 to *timed_out (host-mapped) and returns.
+// max_lead: a flag above target + max_lead is a protocol violation (code 2 in timed_out); ~0 disables the check.
 void launch_wait_flags(FlagList flags, int n, unsigned long long target, unsigned long long timeout_ns,
-                       volatile int* timed_out, cudaStream_t st, LaunchCounter& lc);
+                       volatile int* timed_out, cudaStream_t st, LaunchCounter& lc,
+                       unsigned long long max_lead = ~0ull);
 // System-scope release store of `value` after all prior work of the stream.
 void launch_signal_flag(unsigned long long* flag, unsigned long long value, cudaStream_t st, LaunchCounter& lc);
 // Device-side sleep for the injected io / link delays (executors.hpp:213-216).

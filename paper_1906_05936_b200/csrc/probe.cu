@@ -182,3 +182,31 @@ extern "C" int lsgd_b200_test_exchange_kernel(int32_t kind, int32_t n_dev, int32
     return LSGD_B200_ERR_RUNTIME;
   }
 }
+
+// The flag-protocol check of wait_flags_kernel on one device: a flag holding `value`, waited for `target` with
+// `max_lead`; *code = 0 (passed), 2 (protocol violation reported), 1 (timed out after 50 ms).
+extern "C" int lsgd_b200_test_wait_flag(uint64_t value, uint64_t target, uint64_t max_lead, int32_t* code) {
+  try {
+    LSGD_CUDA(cudaSetDevice(0));
+    unsigned long long* f = nullptr;
+    LSGD_CUDA(cudaMalloc(&f, sizeof(unsigned long long)));
+    LSGD_CUDA(cudaMemcpy(f, &value, sizeof(value), cudaMemcpyHostToDevice));
+    int* h = nullptr;
+    LSGD_CUDA(cudaHostAlloc(&h, sizeof(int), cudaHostAllocMapped));
+    *h = 0;
+    int* d = nullptr;
+    LSGD_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+    FlagList fl{};
+    fl.f[0] = f;
+    LaunchCounter lc;
+    launch_wait_flags(fl, 1, target, 50000000ull, d, 0, lc, max_lead);
+    LSGD_CUDA(cudaDeviceSynchronize());
+    *code = *h;
+    cudaFreeHost(h);
+    cudaFree(f);
+    return LSGD_B200_OK;
+  } catch (const std::exception& e) {
+    last_error_slot() = e.what();
+    return LSGD_B200_ERR_RUNTIME;
+  }
+}

@@ -715,6 +715,9 @@ class RankImpl final : public Rank {
     if (!*timed_out_host_) return;
     if (nccl_aborted_.load())
       throw TransportError(cat(nccl_abort_reason_, " on device ", dev_, "; communicators aborted"));
+    if (*timed_out_host_ == 2)
+      throw TransportError(cat("flag protocol violation on device ", dev_,
+                               ": a producer ran ahead of its consumer (buffer reuse before it was read)"));
     throw TransportError(cat("collective timeout or abort on device ", dev_, " after ", spec_.c.collective_timeout_s,
                              " s waiting for peer flags"));
   }
@@ -1267,12 +1270,16 @@ class RankImpl final : public Rank {
   unsigned long long* peer_flag_word(int wid, int idx) const {
     return reinterpret_cast<unsigned long long*>(base(wid) + geo_.peer.flags) + idx;
   }
-  void wait_own(Worker& w, int first, int n_words, int skip, unsigned long long target, cudaStream_t st) {
+  // max_lead (protocol check, wait_flags_kernel): stage and gfull are single-buffered and their producers are gated
+  // by this consumer's own progress, so a staged / arrived flag is never above the round waited for (lead 0);
+  // gstage is double-buffered by round parity (lead 1).
+  void wait_own(Worker& w, int first, int n_words, int skip, unsigned long long target, cudaStream_t st,
+                unsigned long long max_lead) {
     FlagList fl{};
     int n = 0;
     for (int q = 0; q < n_words; ++q)
       if (q != skip) fl.f[n++] = w.flags + first + q;
-    if (n) launch_wait_flags(fl, n, target, timeout_ns(), timed_out_dev_, st, lc_);
+    if (n) launch_wait_flags(fl, n, target, timeout_ns(), timed_out_dev_, st, lc_, max_lead);
   }
   void exchange_push_bucket(Worker& w, int b, int64_t t, cudaStream_t st) {
     tag_ = b;
@@ -1282,7 +1289,7 @@ class RankImpl final : public Rank {
     const auto members = group_members(w.g);
     const int me = w.j;
     if (k_ > 1 && fused_scatter()) {
-      wait_own(w, kStaged + b * kMaxPeers, k_, me, round, st);  // the producers already scattered (main stream)
+      wait_own(w, kStaged + b * kMaxPeers, k_, me, round, st, 0);  // the producers already scattered (main stream)
     } else if (k_ > 1) {
       SrcList<T> src{};
       DstList<T> dst{};
@@ -1305,7 +1312,7 @@ class RankImpl final : public Rank {
         }
       }
       launch_signal_many(sl, n, round, st, lc_);
-      wait_own(w, kStaged + b * kMaxPeers, k_, me, round, st);
+      wait_own(w, kStaged + b * kMaxPeers, k_, me, round, st, 0);
     }
     SrcList<T> src{};
     for (int m = 0; m < k_; ++m)
@@ -1347,7 +1354,7 @@ class RankImpl final : public Rank {
           launch_reduce_push<T>(src, k_, bk.S, gdst, n, lsgd, static_cast<T>(N_), st, lc_);
         }
         launch_signal_many(gsig, n, round, st, lc_);
-        wait_own(w, kGsum + b * kMaxPeers, G_, w.g, round, st);
+        wait_own(w, kGsum + b * kMaxPeers, G_, w.g, round, st, 1);
       }
       // K7 + broadcast to the other members + K8 of this owner's slot in one pass
       GlobalUpdateArgs<T> ga;
@@ -1447,7 +1454,8 @@ class RankImpl final : public Rank {
       int nf = 0;
       for (int j = 0; j < k_; ++j)
         if (!own || j != w.j) fl.f[nf++] = peer_arrived(w.id, b, j);
-      if (nf) launch_wait_flags(fl, nf, static_cast<unsigned long long>(u + 1), timeout_ns(), timed_out_dev_, st, lc_);
+      if (nf)
+        launch_wait_flags(fl, nf, static_cast<unsigned long long>(u + 1), timeout_ns(), timed_out_dev_, st, lc_, 0);
       a.slices.p[0] = w.gfull + bk.poff;
       a.slice_len = bk.S * k_;
       if (own) {

@@ -331,3 +331,18 @@ def test_loss_history_longer_than_the_device_ring():
     assert long.loss_history.shape == (70_000,) and np.isfinite(long.loss_history).all()
     assert np.array_equal(long.loss_history[:300], short.loss_history)  # same rounds, same bits (deterministic)
     assert not np.array_equal(long.loss_history[65_536:65_836], long.loss_history[:300])  # not wrapped
+
+
+def test_flag_protocol_check():
+    """wait_flags_kernel's round-counter check (the stand-in for compute-sanitizer, which is closed on this pool):
+    a flag at the awaited round passes, one a round beyond the allowed lead is reported as a protocol violation
+    (code 2 -> TransportError in the engine), one below the target times out (code 1)."""
+    import ctypes as C
+    from paper_1906_05936_b200 import _native as N
+    f = N.lib.lsgd_b200_test_wait_flag
+    f.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(C.c_int32)]
+    f.restype = C.c_int
+    code = C.c_int32()
+    for value, target, lead, want in [(5, 5, 0, 0), (6, 5, 1, 0), (6, 5, 0, 2), (7, 5, 1, 2), (4, 5, 0, 1)]:
+        N.check(f(value, target, lead, C.byref(code)))
+        assert code.value == want, (value, target, lead, code.value)
