@@ -384,7 +384,7 @@ __global__ void wait_flags_kernel(FlagList fl, int n, unsigned long long target,
       unsigned long long v;
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(fl.f[i]) : "memory");
       if (v >= target) {
-        if (v > target + max_lead) {
+        if (v - target > max_lead) {  // (no overflow for max_lead = ~0: check disabled)
           *timed_out = 2;
           __threadfence_system();
         }
