@@ -132,6 +132,12 @@ int lsgd_b200_run_train(const lsgd_b200_config* cfg, lsgd_b200_result* out);
 typedef struct lsgd_b200_rank lsgd_b200_rank;
 /* Create worker `rank` (0..N-1) on CUDA device `device`; allocates its peer-visible payload/slice buffers. */
 int lsgd_b200_rank_create(const lsgd_b200_config* cfg, int32_t rank, int32_t device, lsgd_b200_rank** out);
+/* The caller's dataset for this rank (run_rank(cfg, const Dataset& data, ...), executors.hpp:143-144): x
+ * [n_samples * n_features] row-major float64 (Dataset::features), y [n_samples] (Dataset::labels), replacing the
+ * synthetic blobs the rank was created with. n_samples must equal cfg->n_samples (the sampler's range), n_features
+ * cfg->n_features, labels in [0, n_classes): ConfigError otherwise. Call before the first step. */
+int lsgd_b200_rank_upload_dataset(lsgd_b200_rank* r, const double* x, const int32_t* y, int64_t n_samples,
+                                  int32_t n_features);
 /* Bytes this rank must publish to every other rank (CUDA IPC handle + NCCL unique id for its slice comm). */
 int lsgd_b200_rank_blob_size(int64_t* out);
 int lsgd_b200_rank_export(lsgd_b200_rank* r, void* blob);

@@ -78,6 +78,7 @@ _SIGNATURES = {
     "lsgd_b200_rank_blob_size": ([_P], C.c_int),
     "lsgd_b200_rank_export": ([_P, _P], C.c_int),
     "lsgd_b200_rank_connect": ([_P, _P], C.c_int),
+    "lsgd_b200_rank_upload_dataset": ([_P, _P, _P, C.c_int64, C.c_int32], C.c_int),
     "lsgd_b200_rank_step": ([_P, C.c_int64, _P], C.c_int),
     "lsgd_b200_rank_step_rows": ([_P, C.c_int64, _P, _P], C.c_int),
     "lsgd_b200_rank_drain": ([_P], C.c_int),

@@ -232,6 +232,23 @@ int lsgd_b200_rank_create(const lsgd_b200_config* c, int32_t rank, int32_t devic
   });
 }
 
+int lsgd_b200_rank_upload_dataset(lsgd_b200_rank* r, const double* x, const int32_t* y, int64_t n_samples,
+                                  int32_t n_features) {
+  return guarded([&] {
+    const RunSpec& s = *r->spec;
+    check<ConfigError>(s.c.model == LSGD_B200_MODEL_MLP, "upload_dataset: the synthetic-gradient model has no data");
+    check<ConfigError>(n_features == s.c.n_features, "upload_dataset: dataset has ", n_features,
+                       " features, model.layer_sizes[0] is ", s.c.n_features);
+    // the sampler draws from data.n_samples (executors.cpp:73, sampler.cpp:15-43): the config must say the size
+    check<ConfigError>(n_samples == s.c.n_samples, "upload_dataset: dataset has ", n_samples,
+                       " samples, the config's data.n_samples is ", s.c.n_samples);
+    for (int64_t i = 0; i < n_samples; ++i)
+      check<ConfigError>(y[i] >= 0 && y[i] < s.c.n_classes, "upload_dataset: label ", y[i], " of sample ", i,
+                         " is outside [0, ", s.c.n_classes, ")");
+    r->rank->upload_dataset(x, y, n_samples);
+  });
+}
+
 int lsgd_b200_rank_blob_size(int64_t* out) {
   *out = kBlobBytes;
   return LSGD_B200_OK;

@@ -446,6 +446,18 @@ class RankImpl final : public Rank {
     const int d = spec_.c.n_features;
     std::vector<T> conv(static_cast<size_t>(n) * d);
     for (size_t i = 0; i < conv.size(); ++i) conv[i] = static_cast<T>(x[i]);
+    if (own_data_) {  // a caller-supplied dataset replaces the one created with the rank
+      LSGD_CUDA(cudaStreamSynchronize(main_));
+      if (host_data_) LSGD_CUDA(cudaFreeHost(host_alloc_));
+      else {
+        LSGD_CUDA(cudaFree(data_x_));
+        LSGD_CUDA(cudaFree(data_y_));
+      }
+      host_alloc_ = nullptr;
+      data_x_ = nullptr;
+      data_y_ = nullptr;
+      host_data_ = false;
+    }
     own_data_ = true;
     n_rows_ = n;
     if (spec_.c.data_source == LSGD_B200_DATA_HOST) {

@@ -264,6 +264,14 @@ class Rank:
         allb = b"".join(blobs)
         N.check(N.lib.lsgd_b200_rank_connect(self.h, C.c_char_p(allb)))
 
+    def upload_dataset(self, x: np.ndarray, y: np.ndarray) -> None:
+        """The caller's dataset (run_rank's `const Dataset&`, executors.hpp:143-144): x [n, d] float64, y [n]."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.int32)
+        if x.ndim != 2 or y.shape != (x.shape[0],):
+            raise N.ConfigError(f"upload_dataset: x must be [n, d] and y [n], got {x.shape} and {y.shape}")
+        N.check(N.lib.lsgd_b200_rank_upload_dataset(self.h, x.ctypes.data, y.ctypes.data, x.shape[0], x.shape[1]))
+
     def step(self, n: int = 1, shard_indices: Optional[np.ndarray] = None) -> None:
         p = None
         if shard_indices is not None:

@@ -169,3 +169,42 @@ def test_missing_peer_on_nccl_is_a_transport_error_not_a_hang(over, n_gpus):
         pytest.skip("needs 2 GPUs")
     out = _spawn(2, "fp64", 1 if over is FLAT else 2, "timeout", over=over)
     assert out["err"] == "TransportError", out
+
+
+def test_caller_dataset_through_upload_dataset(n_gpus):
+    """run_rank(cfg, const Dataset&, ...) (executors.hpp:143-144) -> lsgd_b200_rank_upload_dataset: uploading the very
+    blobs the rank generated gives bitwise the same training; a different dataset gives different iterates; shape and
+    label errors are ConfigErrors (dataset.cpp's checks)."""
+    import paper_1906_05936_b200 as lsgd
+    from paper_1906_05936_b200 import host
+    from paper_1906_05936_b200.executors import Rank
+
+    def train(data=None):
+        cfg = _cfg("fp64", 1, 1)
+        r = Rank(cfg, 0, 0)
+        r.connect([r.export()])
+        if data is not None:
+            r.upload_dataset(*data)
+        r.step(cfg.iterations)
+        r.drain()
+        w = r.params()
+        r.close()
+        return w
+
+    cfg = _cfg("fp64", 1, 1)
+    x, y = host.generate_synthetic(cfg.seed, cfg.n_samples, cfg.n_features, cfg.n_classes, cfg.spread)
+    base = train()
+    same = train((x, y))
+    assert np.array_equal(base.view(np.uint64), same.view(np.uint64))
+    other = train((x[::-1].copy(), y[::-1].copy()))
+    assert not np.array_equal(base, other)
+    r = Rank(cfg, 0, 0)
+    with pytest.raises(lsgd.ConfigError):
+        r.upload_dataset(x[:, :-1], y)
+    with pytest.raises(lsgd.ConfigError):
+        r.upload_dataset(x[:-1], y[:-1])
+    bad = y.copy()
+    bad[3] = cfg.n_classes
+    with pytest.raises(lsgd.ConfigError):
+        r.upload_dataset(x, bad)
+    r.close()
