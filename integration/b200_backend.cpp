@@ -1,0 +1,221 @@
+// The reference-side binding a maintainer adds to route the reference's trainer through liblsgd_b200.so
+// (INTEGRATION.md §1): `transport.backend = "b200"` selects these instead of the in-process / TCP executors.
+//
+//   lsgd::run_train_b200          replaces lsgd::run_train          (include/lsgd/executors.hpp:138,
+//                                                                     src/executors.cpp:481-521)
+//   lsgd::verify_equivalence_b200 replaces lsgd::verify_equivalence (executors.hpp:163, executors.cpp:523-587)
+//
+// Compiled against the reference's own headers (/root/reference/proj/include) and linked with the reference's
+// sources and -llsgd_b200 by oracle/Makefile (target `acceptance`), which also builds the reference's unmodified
+// acceptance suite (proj/tests/acceptance.cpp) with integration/b200_redirect.hpp force-included, so its
+// criteria that train (1 iterate equivalence, 2 degenerate bitwise, 4 io/allreduce overlap, 8 convergence) run on
+// the B200 path. Parity mode: LSGD_B200_DTYPE=fp64 (default here, the reference's arithmetic) or fp32.
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "lsgd/executors.hpp"
+#include "lsgd_b200.h"
+
+namespace lsgd {
+
+namespace {
+
+[[noreturn]] void throw_b200(int rc) {
+  std::string msg = lsgd_b200_last_error();
+  if (rc == LSGD_B200_ERR_CONFIG) throw ConfigError(msg);
+  if (rc == LSGD_B200_ERR_TRANSPORT) throw TransportError(msg);
+  throw Error(msg);
+}
+
+int32_t b200_dtype() {
+  const char* e = std::getenv("LSGD_B200_DTYPE");
+  return (e && std::strcmp(e, "fp32") == 0) ? LSGD_B200_FP32 : LSGD_B200_FP64;
+}
+
+}  // namespace
+
+TrainResult run_train_b200(const TrainConfig& cfg) {
+  cfg.validate();
+  check<ConfigError>(cfg.data.source == DataSpec::Source::synthetic,
+                     "transport.backend = b200: data.source must be synthetic (csv ingestion is not on the step)");
+  lsgd_b200_config c;
+  if (int rc = lsgd_b200_config_init(&c)) throw_b200(rc);
+  std::vector<int32_t> layers(cfg.model.layer_sizes.begin(), cfg.model.layer_sizes.end());
+  c.algorithm = static_cast<int32_t>(cfg.algorithm);  // same enum order (executors.hpp:17)
+  c.n_workers = cfg.topology.n_workers;
+  c.n_groups = cfg.topology.n_groups;
+  c.n_layers = static_cast<int32_t>(layers.size());
+  c.layer_sizes = layers.data();
+  c.n_samples = cfg.data.n_samples;
+  c.n_features = cfg.data.n_features;
+  c.n_classes = cfg.data.n_classes;
+  c.spread = cfg.data.spread;
+  c.mode = cfg.optim.mode == UpdateMode::plain ? LSGD_B200_PLAIN : LSGD_B200_MOMENTUM;
+  c.base_lr = cfg.optim.base_lr;
+  c.momentum = cfg.optim.momentum;
+  c.weight_decay = cfg.optim.weight_decay;
+  c.warmup_epochs = cfg.optim.warmup_epochs;
+  c.decay_every_epochs = cfg.optim.decay_every_epochs;
+  c.decay_factor = cfg.optim.decay_factor;
+  c.local_batch = cfg.local_batch;
+  c.epochs = cfg.epochs;
+  c.iterations = cfg.iterations;
+  c.seed = cfg.seed;
+  c.init_scale = cfg.init_scale;
+  c.io_delay_s = cfg.delays.io_delay_s;
+  c.global_link_delay_s = cfg.delays.global_link_delay_s;
+  c.collective_timeout_s = cfg.collective_timeout_s;
+  c.record_history = cfg.record_history ? 1 : 0;
+  c.shared_minibatch = cfg.shared_minibatch ? 1 : 0;
+  c.dtype = b200_dtype();
+  c.record_phases = 1;  // the reference always records per-rank phase spans (executors.hpp:85-102)
+
+  const int64_t T = cfg.resolve_iterations(cfg.data.n_samples);
+  const int64_t P = cfg.model.n_params();
+  const int N = cfg.topology.n_workers;
+  const size_t uT = static_cast<size_t>(T), uP = static_cast<size_t>(P);
+  std::vector<double> final_params(uP), loss(uT), lr(uT), hist, finals(static_cast<size_t>(N) * uP);
+  std::vector<int64_t> version(static_cast<size_t>(N) * uT);
+  std::vector<double> spans(static_cast<size_t>(N) * uT * 12);
+  if (cfg.record_history) hist.resize((uT + 1) * uP);
+  lsgd_b200_result out{};
+  out.final_params = final_params.data();
+  out.loss = loss.data();
+  out.lr = lr.data();
+  out.history = cfg.record_history ? hist.data() : nullptr;
+  out.worker_finals = finals.data();
+  out.version_at_compute = version.data();
+  out.phase_spans = spans.data();
+  if (int rc = lsgd_b200_run_train(&c, &out)) throw_b200(rc);
+
+  auto span = [&](int w, int64_t t, int p) {
+    const double* s = spans.data() + ((static_cast<size_t>(w) * uT + static_cast<size_t>(t)) * 6 + p) * 2;
+    PhaseSpan ps;
+    ps.begin = s[0];
+    ps.end = s[1];
+    return ps;
+  };
+
+  // per-rank results in the reference's layout: workers 0..N-1, then (LSGD) one communicator per group, whose
+  // local_reduce / global_allreduce / broadcast spans are those of the group's exchange (recorded on the comm
+  // stream of the group's first worker, which owns slot 0 of every bucket)
+  const int G = cfg.topology.n_groups, k = N / G;
+  const bool lsgd = cfg.algorithm == Algorithm::lsgd;
+  TrainResult r;
+  r.initial_params = init_params(cfg.model, Rng(cfg.seed + 1), cfg.init_scale);
+  r.final_params = final_params;
+  r.loss_history = loss;
+  const int world = lsgd ? N + G : N;
+  r.ranks.resize(static_cast<size_t>(world));
+  for (int rank = 0; rank < world; ++rank) {
+    RankResult& rr = r.ranks[static_cast<size_t>(rank)];
+    rr.rank = rank;
+    const bool comm = lsgd && rank >= N;
+    rr.role = comm ? Role::communicator : Role::worker;
+    const int src = comm ? (rank - N) * k : rank;
+    rr.iterations.resize(uT);
+    for (int64_t t = 0; t < T; ++t) {
+      RankIteration& it = rr.iterations[static_cast<size_t>(t)];
+      for (int p = 0; p < 6; ++p) {
+        const bool comm_phase = p == static_cast<int>(TrainPhase::local_reduce) ||
+                                p == static_cast<int>(TrainPhase::global_allreduce) ||
+                                p == static_cast<int>(TrainPhase::broadcast);
+        if (comm && !comm_phase) continue;
+        it.phase[static_cast<size_t>(p)] = span(src, t, p);
+      }
+      if (!comm) it.version_at_compute = version[static_cast<size_t>(rank) * uT + static_cast<size_t>(t)];
+      double b = 1e300, e = 0.0;
+      for (const PhaseSpan& ps : it.phase)
+        if (ps.present()) {
+          b = std::min(b, ps.begin);
+          e = std::max(e, ps.end);
+        }
+      it.block_begin = b < 1e300 ? b : 0.0;
+      it.block_end = e;
+    }
+    if (!comm) {
+      rr.loss = loss;
+      rr.lr = lr;
+      rr.final_params.assign(finals.begin() + static_cast<std::ptrdiff_t>(rank) * P,
+                             finals.begin() + static_cast<std::ptrdiff_t>(rank + 1) * P);
+    }
+    rr.total_wall_s = out.total_wall_s;
+  }
+  r.rows.resize(uT);
+  for (int64_t t = 0; t < T; ++t) {  // merge_results (executors.cpp:336-355)
+    IterationRow& row = r.rows[static_cast<size_t>(t)];
+    const RankIteration& it = r.ranks[0].iterations[static_cast<size_t>(t)];
+    row.lr = lr[static_cast<size_t>(t)];
+    row.loss = loss[static_cast<size_t>(t)];
+    row.phase = it.phase;
+    row.iter_wall_s = it.block_end - it.block_begin;
+    if (lsgd) {
+      PhaseSpan widest{};
+      for (int g = 0; g < G; ++g) {
+        const PhaseSpan& s = r.ranks[static_cast<size_t>(N + g)].iterations[static_cast<size_t>(t)].phase[
+            static_cast<size_t>(TrainPhase::global_allreduce)];
+        if (s.duration() > widest.duration()) widest = s;
+      }
+      row.phase[static_cast<size_t>(TrainPhase::global_allreduce)] = widest;
+    }
+  }
+  for (int64_t t = 0; cfg.record_history && t <= T; ++t)
+    r.param_history.emplace_back(hist.begin() + static_cast<std::ptrdiff_t>(t) * P,
+                                 hist.begin() + static_cast<std::ptrdiff_t>(t + 1) * P);
+  r.total_wall_s = out.total_wall_s;
+  r.throughput_sps = out.throughput_sps;
+  return r;
+}
+
+// verify_equivalence (executors.cpp:523-587) with every run on the B200 backend: the same config checks, the same
+// coordinate-wise |a-b| / max(|a|, 1e-8) metric against the first config's iterates.
+EquivalenceReport verify_equivalence_b200(const std::vector<TrainConfig>& configs, double tolerance) {
+  check<ConfigError>(configs.size() >= 2, "verify: need at least two configs");
+  const TrainConfig& ref = configs.front();
+  for (const TrainConfig& cfg : configs) {
+    cfg.validate();
+    check<ConfigError>(cfg.optim.mode == UpdateMode::plain, "verify: iterate comparison requires optim.mode = plain");
+    check<ConfigError>(cfg.shared_minibatch, "verify: iterate comparison requires the shared-minibatch mode");
+    check<ConfigError>(cfg.seed == ref.seed, "verify: configs disagree on seed");
+    check<ConfigError>(cfg.model.layer_sizes == ref.model.layer_sizes, "verify: configs disagree on model.layer_sizes");
+    check<ConfigError>(cfg.global_batch() == ref.global_batch(), "verify: configs disagree on global batch");
+    check<ConfigError>(cfg.epochs == ref.epochs && cfg.iterations == ref.iterations,
+                       "verify: configs disagree on iteration count");
+  }
+  EquivalenceReport report;
+  report.tolerance = tolerance;
+  std::vector<std::vector<ParamVector>> hists;
+  for (const TrainConfig& cfg : configs) {
+    TrainConfig recording = cfg;
+    recording.record_history = true;
+    hists.push_back(run_train_b200(recording).param_history);
+  }
+  report.pass = true;
+  for (size_t i = 0; i < configs.size(); ++i) {
+    EquivalenceEntry entry;
+    entry.name = str_cat(algorithm_name(configs[i].algorithm), " N=", configs[i].topology.n_workers,
+                         " G=", configs[i].topology.n_groups, " (b200)");
+    check<ConfigError>(hists[i].size() == hists[0].size(), "verify: iterate history length mismatch");
+    entry.bitwise_equal = true;
+    for (size_t t = 0; t < hists[i].size(); ++t) {
+      const ParamVector& a = hists[0][t];
+      const ParamVector& b = hists[i][t];
+      for (size_t q = 0; q < a.size(); ++q) {
+        if (std::memcmp(&a[q], &b[q], sizeof(double)) != 0) entry.bitwise_equal = false;
+        const double dev = std::abs(a[q] - b[q]) / std::max(std::abs(a[q]), 1e-8);
+        if (dev > entry.max_rel_deviation) {
+          entry.max_rel_deviation = dev;
+          entry.worst_iteration = static_cast<int64_t>(t);
+        }
+      }
+    }
+    if (i > 0 && entry.max_rel_deviation > tolerance) report.pass = false;
+    report.entries.push_back(std::move(entry));
+  }
+  return report;
+}
+
+}  // namespace lsgd
