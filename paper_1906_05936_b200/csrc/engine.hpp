@@ -95,6 +95,9 @@ class Rank {
   virtual void issue_steps(int64_t n, const int32_t* host_global_or_shard_indices, bool shard_only) = 0;
   virtual void issue_steps_rows(int64_t n, const void* x_host, const int32_t* y_host) = 0;
   virtual void drain() = 0;
+  // version_at_compute (executors.hpp:102), measured on the device: for each iteration t < n, the number of update
+  // rounds every layer had received when the forward pass of t read it (min over layers). -1 where not tracked.
+  virtual void versions(int worker, int64_t* out, int64_t n) = 0;
   virtual void synchronize() = 0;
   virtual int64_t steps_issued() const = 0;
   virtual int64_t updates_applied() const = 0;

@@ -603,6 +603,13 @@ __global__ void __launch_bounds__(256) global_update_kernel(const __grid_constan
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x % 32) == 0) atomicOr(a.bad, 1u);
 }
 
+__global__ void store_u64_kernel(unsigned long long* p, unsigned long long v) { *p = v; }
+__global__ void min_u64_kernel(const unsigned long long* ver, int b0, int b1, long long* dst) {
+  unsigned long long m = ~0ull;
+  for (int b = b0; b < b1; ++b) m = min(m, ver[b]);
+  *dst = static_cast<long long>(m);
+}
+
 __global__ void signal_many_kernel(SignalList fl, int n, unsigned long long v) {
   __threadfence_system();
   if (threadIdx.x < n) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(fl.f[threadIdx.x]), "l"(v) : "memory");
@@ -728,6 +735,18 @@ void launch_update(const UpdateArgs<T>& a_in, bool exact, cudaStream_t st, Launc
     else LSGD_UPD(false, 2);
   }
 #undef LSGD_UPD
+  ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
+}
+
+void launch_store_u64(unsigned long long* ver, unsigned long long value, cudaStream_t st, LaunchCounter& lc) {
+  store_u64_kernel<<<1, 1, 0, st>>>(ver, value);
+  ++lc.n;
+  LSGD_CUDA(cudaGetLastError());
+}
+void launch_min_u64(const unsigned long long* ver, int b0, int b1, long long* dst, cudaStream_t st,
+                    LaunchCounter& lc) {
+  min_u64_kernel<<<1, 1, 0, st>>>(ver, b0, b1, dst);
   ++lc.n;
   LSGD_CUDA(cudaGetLastError());
 }

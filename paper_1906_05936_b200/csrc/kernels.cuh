@@ -139,6 +139,11 @@ struct FlagList {
 void launch_wait_flags(FlagList flags, int n, unsigned long long target, unsigned long long timeout_ns,
                        volatile int* timed_out, cudaStream_t st, LaunchCounter& lc,
                        unsigned long long max_lead = ~0ull);
+// Version tracking (executors.hpp:102 version_at_compute, measured): `*ver = value` after the prior work of the
+// stream, and `*dst = min ver[b0..b1)` (the oldest update any of a layer's buckets has received when its forward
+// reads it). One thread each.
+void launch_store_u64(unsigned long long* ver, unsigned long long value, cudaStream_t st, LaunchCounter& lc);
+void launch_min_u64(const unsigned long long* ver, int b0, int b1, long long* dst, cudaStream_t st, LaunchCounter& lc);
 // System-scope release store of `value` after all prior work of the stream.
 void launch_signal_flag(unsigned long long* flag, unsigned long long value, cudaStream_t st, LaunchCounter& lc);
 // Device-side sleep for the injected io / link delays (executors.hpp:213-216).

@@ -760,6 +760,8 @@ class RankImpl final : public Rank {
     std::vector<T*> dl;  // delta of each layer [B, out_k]
     T* sample_loss = nullptr;
     T* loss_hist = nullptr;
+    unsigned long long* ver = nullptr;  // [kMaxBuckets] update rounds applied per bucket (version tracking)
+    long long* ver_log = nullptr;       // host-mapped [T * depth]: per iteration and layer, read at its forward
     TcWorkspace tc;  // split-TF32 operands of the tensor-core path
     bool x_split_ready = false;  // io() gathered this step's rows straight into the TC split
     const PeerLayout* lay = nullptr;
@@ -781,6 +783,13 @@ class RankImpl final : public Rank {
     w.id = wid;
     w.g = wid / k_;
     w.j = wid % k_;
+    if (track_versions()) {
+      LSGD_CUDA(cudaMalloc(&w.ver, sizeof(unsigned long long) * kMaxBuckets));
+      LSGD_CUDA(cudaMemsetAsync(w.ver, 0, sizeof(unsigned long long) * kMaxBuckets, main_));
+      const size_t n = static_cast<size_t>(spec_.iterations()) * static_cast<size_t>(L_.depth());
+      LSGD_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&w.ver_log), sizeof(long long) * n, cudaHostAllocMapped));
+      for (size_t i = 0; i < n; ++i) w.ver_log[i] = -1;
+    }
     LSGD_CUDA(cudaMalloc(&w.blk, static_cast<size_t>(geo_.peer.total)));
     LSGD_CUDA(cudaMemsetAsync(w.blk, 0, static_cast<size_t>(geo_.peer.total), main_));
     w.flags = reinterpret_cast<unsigned long long*>(w.blk + geo_.peer.flags);
@@ -831,6 +840,8 @@ class RankImpl final : public Rank {
   }
 
   void free_worker(Worker& w) {
+    if (w.ver) cudaFree(w.ver);
+    if (w.ver_log) cudaFreeHost(w.ver_log);
     cudaFree(w.blk);
     cudaFree(w.w);
     if (w.v) cudaFree(w.v);
@@ -1070,6 +1081,33 @@ class RankImpl final : public Rank {
   }
   // One worker, one group (N = 1): the gradient is final when produced, so the update runs in the producers'
   // epilogues (dW GEMM, bias) and the separate update pass over g disappears.
+  // Measured version_at_compute: on for recorded runs of bounded length (run_train with history / phases), off
+  // for the bench and the open-ended rank API (two 1-thread kernels per bucket and layer per step).
+  bool track_versions() const {
+    return !synth_ && (hist_rows_ > 0 || spec_.c.record_phases) && spec_.iterations() <= (1 << 20) &&
+           !fused_update();
+  }
+  void note_version(Worker& w, int b, int64_t rounds, cudaStream_t st) {
+    if (w.ver) launch_store_u64(w.ver + b, static_cast<unsigned long long>(rounds), st, lc_);
+  }
+  void versions(int worker, int64_t* out, int64_t n) override {
+    synchronize();
+    Worker& w = find(worker);
+    const int D = L_.depth();
+    for (int64_t t = 0; t < n; ++t) {
+      if (!w.ver_log || t >= spec_.iterations()) {
+        out[t] = -1;
+        continue;
+      }
+      long long m = -1;
+      for (int k = 0; k < D; ++k) {
+        const long long v = w.ver_log[t * D + k];
+        m = (k == 0 || v < m) ? v : m;
+      }
+      out[t] = m;
+    }
+  }
+
   bool fused_update() const {
     // opt-in (LSGD_B200_FUSED_UPDATE=1): bitwise the separate pass, but its epilogue is latency-bound today
     static const bool on = std::getenv("LSGD_B200_FUSED_UPDATE") != nullptr;
@@ -1539,8 +1577,15 @@ class RankImpl final : public Rank {
           } else if (postponed) {
             current_phase() = "broadcast";
             apply_bucket(w, b, t - 1, main_);
+            note_version(w, b, t, main_);
             current_phase() = "compute";
           }
+        }
+        if (w.ver_log) {  // the update rounds layer k's parameters have received when this forward reads them
+          const auto& lb = LB[static_cast<size_t>(k)];
+          long long* dst = nullptr;
+          LSGD_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dst), w.ver_log + t * D + k, 0));
+          launch_min_u64(w.ver, lb.front(), lb.back() + 1, dst, main_, lc_);
         }
         forward_layer(w, k);
       }
@@ -1685,6 +1730,7 @@ class RankImpl final : public Rank {
           if (reduce_folded() && bias_side_[b]) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_bias_[b], 0));
           apply_bucket(w, b, t, upd_);
           if (own_slot_fused()) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_gupd_[b], 0));  // own slot (comm stream)
+          note_version(w, b, t + 1, upd_);
           LSGD_CUDA(cudaEventRecord(ev_upd_[b], upd_));
         }
       }
@@ -1698,6 +1744,7 @@ class RankImpl final : public Rank {
         for (int b = 0; b < NB; ++b) {
           apply_bucket(w, b, t, main_);
           if (own_slot_fused()) LSGD_CUDA(cudaStreamWaitEvent(main_, ev_gupd_[b], 0));
+          note_version(w, b, t + 1, main_);
         }
         after_update(w, t, main_);
       }

@@ -188,8 +188,9 @@ void run_world(const RunSpec& spec, bool want_history, bool want_workers, TrainO
     for (auto& r : ranks)
       for (int w : r->workers()) {
         r->get_params(w, out.worker_finals.data() + static_cast<int64_t>(w) * P);
-        // stream order makes gradient t read w_t: t updates were applied before compute t (executors.cpp:245)
-        for (int64_t t = 0; t < T; ++t) out.version_at_compute[static_cast<size_t>(w * T + t)] = t;
+        // measured on the device: the update rounds every layer had received when the forward of t read it
+        // (executors.cpp:244 records opt.iteration at the gradient pass)
+        r->versions(w, out.version_at_compute.data() + static_cast<int64_t>(w) * T, T);
       }
   }
   if (spec.c.record_phases) {
