@@ -1250,6 +1250,21 @@ class RankImpl final : public Rank {
     backward_input(w, k);
   }
 
+  // The global stage of the push exchange sliced over the G owners of each slot (reduce-scatter + all-gather, see
+  // exchange_push_bucket). LSGD_B200_SLICED_GLOBAL = 0 / 1 forces it; default: on for G > 2, where the whole-slot
+  // form's (G-1) slot lengths of egress per owner dominate.
+  bool sliced_global() const {
+    static const char* e = std::getenv("LSGD_B200_SLICED_GLOBAL");
+    if (G_ <= 1 || !own_slot_fused() || N_ > kMaxPeers) return false;  // one arrived word per source owner
+    if (e) return std::atoi(e) != 0;
+    return G_ > 2;
+  }
+  int64_t piece_len(const Bucket& bk) const {  // elements of each of the G pieces of a slot (64-aligned)
+    return sliced_global() ? round_up((bk.S + G_ - 1) / G_, kAlign) : bk.S;
+  }
+  // arrived flag of the averaged piece (slot j, piece q): one word per source owner
+  int arrived_index(int j, int q) const { return sliced_global() ? j * G_ + q : j; }
+
   std::vector<int> group_members(int g) const {
     std::vector<int> m;
     for (int i = g * k_; i < (g + 1) * k_; ++i) m.push_back(i);
@@ -1375,15 +1390,31 @@ class RankImpl final : public Rank {
     }
     const bool lsgd = alg_ == LSGD_B200_LSGD;
     if (own_slot_fused()) {
-      // G > 1: the slot sum goes to the other groups' slot owners only (this owner recomputes it below)
+      // Sliced global stage (sliced_global()): slot `me` is cut into G pieces; the owner in group q computes the
+      // average of piece q only. Owner (g, me) pushes piece q of its group sum to owner (q, me) (reduce-scatter
+      // over the slot's G owners), sums piece g over the groups in ascending order, updates its parameters of that
+      // piece and pushes its average to all N-1 other GPUs (all-gather). Same per-element arithmetic, so the same
+      // bits as the whole-slot form, at 2(G-1)/G instead of G-1 slot lengths of egress for the global stage.
+      // Unsliced: the piece is the whole slot, the group sum goes to all G-1 other owners and the average to the
+      // k-1 group members.
+      const bool sl = sliced_global();
+      const int64_t Q = piece_len(bk);
+      const int pg = sl ? w.g : 0;                        // the piece this owner averages
+      const int64_t p0 = static_cast<int64_t>(pg) * Q;    // its offset inside the slot
+      const int64_t plen = std::max<int64_t>(0, std::min(Q, bk.S - p0));
+      // G > 1: the slot sum (or, sliced, each other owner's piece of it) goes to the other groups' slot owners
       if (G_ > 1) {
         DstList<T> gdst{};
         SignalList gsig{};
+        int64_t goff_q[kMaxPeers] = {}, glen_q[kMaxPeers] = {};
         int n = 0;
         for (int g = 0; g < G_; ++g) {
           if (g == w.g) continue;
           const int owner = g * k_ + me;
-          gdst.p[n] = peer_gstage(owner, par, w.g) + bk.goff;
+          const int64_t q0 = sl ? static_cast<int64_t>(g) * Q : 0;  // piece g goes to the owner in group g
+          goff_q[n] = q0;
+          glen_q[n] = sl ? std::max<int64_t>(0, std::min(Q, bk.S - q0)) : bk.S;
+          gdst.p[n] = peer_gstage(owner, par, w.g) + bk.goff + q0;
           gsig.f[n++] = peer_flag_word(owner, kGsum + b * kMaxPeers + w.g);
         }
         if (k_ == 1 && dma(1)) {
@@ -1391,14 +1422,28 @@ class RankImpl final : public Rank {
           // the receiving owner applies the group's (+0.0, /N) when it reads it
           Timed tm(this, "reduce", st);
           for (int q = 0; q < n; ++q)
-            LSGD_CUDA(cudaMemcpyAsync(gdst.p[q], src.p[0], sizeof(T) * bk.S, cudaMemcpyDeviceToDevice, st));
+            if (glen_q[q])
+              LSGD_CUDA(cudaMemcpyAsync(gdst.p[q], src.p[0] + goff_q[q], sizeof(T) * glen_q[q],
+                                        cudaMemcpyDeviceToDevice, st));
         } else if (k_ > 1 && dma(4)) {  // the group sum lands locally, the copy engines forward it
           Timed tm(this, "reduce", st);
           DstList<T> loc{};
           loc.p[0] = w.s[par] + bk.goff;
           launch_reduce_push<T>(src, k_, bk.S, loc, 1, lsgd, static_cast<T>(N_), st, lc_);
           for (int q = 0; q < n; ++q)
-            LSGD_CUDA(cudaMemcpyAsync(gdst.p[q], loc.p[0], sizeof(T) * bk.S, cudaMemcpyDeviceToDevice, st));
+            if (glen_q[q])
+              LSGD_CUDA(cudaMemcpyAsync(gdst.p[q], loc.p[0] + goff_q[q], sizeof(T) * glen_q[q],
+                                        cudaMemcpyDeviceToDevice, st));
+        } else if (sl) {  // one ordered-sum launch per destination piece
+          Timed tm(this, "reduce", st);
+          for (int q = 0; q < n; ++q) {
+            if (!glen_q[q]) continue;
+            SrcList<T> ps{};
+            for (int m = 0; m < k_; ++m) ps.p[m] = src.p[m] + goff_q[q];
+            DstList<T> one{};
+            one.p[0] = gdst.p[q];
+            launch_reduce_push<T>(ps, k_, glen_q[q], one, 1, lsgd, static_cast<T>(N_), st, lc_);
+          }
         } else {
           Timed tm(this, "reduce", st);
           launch_reduce_push<T>(src, k_, bk.S, gdst, n, lsgd, static_cast<T>(N_), st, lc_);
@@ -1406,24 +1451,25 @@ class RankImpl final : public Rank {
         launch_signal_many(gsig, n, round, st, lc_);
         wait_own(w, kGsum + b * kMaxPeers, G_, w.g, round, st, 1);
       }
-      // K7 + broadcast to the other members + K8 of this owner's slot in one pass
+      // K7 + broadcast + K8 of this owner's piece (the whole slot unsliced) in one pass
       GlobalUpdateArgs<T> ga;
-      ga.src = src;
+      for (int m = 0; m < k_; ++m) ga.src.p[m] = src.p[m] + p0;
       ga.k = k_;
-      for (int g = 0; g < G_; ++g) ga.gsum.p[g] = w.blk_gstage(par, g) + bk.goff;
+      for (int g = 0; g < G_; ++g) ga.gsum.p[g] = w.blk_gstage(par, g) + bk.goff + p0;
       ga.G = G_;
       ga.g = w.g;
       ga.gsum_raw = G_ > 1 && k_ == 1 && dma(1);
       ga.add_zero = lsgd;
       ga.divisor = static_cast<T>(N_);
-      ga.len = bk.S;
+      ga.len = plen;
       SignalList others{};
-      for (int m = 0; m < k_; ++m) {
-        if (m == me) continue;
-        others.f[ga.n_push] = peer_arrived(members[static_cast<size_t>(m)], b, me);
-        ga.push.p[ga.n_push++] = peer_gfull(members[static_cast<size_t>(m)]) + bk.poff + static_cast<int64_t>(me) * bk.S;
+      const int arr = arrived_index(me, pg);
+      for (int d = 0; d < N_; ++d) {  // sliced: every other GPU; unsliced: the other members of this group
+        if (d == w.id || (!sl && d / k_ != w.g)) continue;
+        others.f[ga.n_push] = peer_arrived(d, b, arr);
+        ga.push.p[ga.n_push++] = peer_gfull(d) + bk.poff + static_cast<int64_t>(me) * bk.S + p0;
       }
-      ga.first = static_cast<int64_t>(me) * bk.S;
+      ga.first = static_cast<int64_t>(me) * bk.S + p0;
       ga.n_params = bk.n;
       ga.w = w.w + bk.pstart;
       ga.v = w.v ? w.v + bk.pstart : nullptr;
@@ -1444,15 +1490,15 @@ class RankImpl final : public Rank {
       const bool fan_dma = dma(8) && n_remote > 0;
       if (fan_dma) {  // average stored locally once, the copy engines fan it out
         ga.n_push = 0;
-        ga.out_local = w.gbar + bk.goff;
+        ga.out_local = w.gbar + bk.goff + p0;
       }
-      {
+      if (plen > 0) {
         Timed tm(this, "global", st);
         launch_global_update<T>(ga, exact_, st, lc_);
       }
-      if (fan_dma)
+      if (fan_dma && plen > 0)
         for (int q = 0; q < n_remote; ++q)
-          LSGD_CUDA(cudaMemcpyAsync(remote.p[q], ga.out_local, sizeof(T) * bk.S, cudaMemcpyDeviceToDevice, st));
+          LSGD_CUDA(cudaMemcpyAsync(remote.p[q], ga.out_local, sizeof(T) * plen, cudaMemcpyDeviceToDevice, st));
       if (n_remote) launch_signal_many(others, n_remote, round, st, lc_);
       LSGD_CUDA(cudaEventRecord(ev_gupd_[b], st));
       return;
@@ -1499,19 +1545,35 @@ class RankImpl final : public Rank {
       }
       if (flat_nccl()) a.post_div = static_cast<T>(N_);  // the per-worker /N after the flat allreduce (:170)
     } else {
-      const bool own = own_slot_fused();  // this worker's own slot was updated by its fused global kernel
-      FlagList fl{};  // the other sub-slices of round u have been pushed into this worker's gfull
-      int nf = 0;
+      const bool own = own_slot_fused();  // this worker's own slot (piece) was updated by its fused global kernel
+      const bool sl = sliced_global();
+      const int n_pieces = sl ? G_ : 1;
+      const int64_t Q = piece_len(bk);
+      const int pg = sl ? w.g : 0;
+      const int64_t p0 = static_cast<int64_t>(pg) * Q;
+      const int64_t plen = std::max<int64_t>(0, std::min(Q, bk.S - p0));
+      // the other (slot, piece) averages of round u have been pushed into this worker's gfull (one flag per
+      // source owner; kMaxPeers words per bucket hold all N of them); waited in chunks of kMaxPeers
+      std::vector<const volatile unsigned long long*> srcs;
       for (int j = 0; j < k_; ++j)
-        if (!own || j != w.j) fl.f[nf++] = peer_arrived(w.id, b, j);
-      if (nf)
+        for (int q = 0; q < n_pieces; ++q) {
+          if (own && j == w.j && q == pg) continue;
+          const int64_t q0 = static_cast<int64_t>(q) * Q;
+          if (sl && std::min(Q, bk.S - q0) <= 0) continue;  // empty trailing piece: nothing is pushed
+          srcs.push_back(peer_arrived(w.id, b, arrived_index(j, q)));
+        }
+      for (size_t i0 = 0; i0 < srcs.size(); i0 += kMaxPeers) {
+        FlagList fl{};
+        int nf = 0;
+        for (size_t i = i0; i < srcs.size() && nf < kMaxPeers; ++i) fl.f[nf++] = srcs[i];
         launch_wait_flags(fl, nf, static_cast<unsigned long long>(u + 1), timeout_ns(), timed_out_dev_, st, lc_, 0);
+      }
       a.slices.p[0] = w.gfull + bk.poff;
       a.slice_len = bk.S * k_;
       if (own) {
-        a.skip_lo = static_cast<int64_t>(w.j) * bk.S;
-        a.skip_hi = a.skip_lo + bk.S;
-        if (k_ == 1) {  // nothing left to update here
+        a.skip_lo = static_cast<int64_t>(w.j) * bk.S + p0;
+        a.skip_hi = a.skip_lo + plen;
+        if (k_ == 1 && n_pieces == 1) {  // nothing left to update here
           if (b == 0) {
             phase_mark(wi, u, 4, 1, st);
             phase_mark(wi, u, 5, 0, st);

@@ -208,3 +208,25 @@ def test_caller_dataset_through_upload_dataset(n_gpus):
     with pytest.raises(lsgd.ConfigError):
         r.upload_dataset(x, bad)
     r.close()
+
+
+@pytest.mark.parametrize("groups,per_group,dtype", [(2, 1, "fp32"), (2, 2, "fp32"), (4, 1, "fp64"), (4, 1, "fp32")])
+def test_sliced_global_is_bitwise_the_whole_slot_form(groups, per_group, dtype, n_gpus):
+    """The global stage sliced over each slot's G owners (reduce-scatter + all-gather; LSGD_B200_SLICED_GLOBAL,
+    default for G > 2) computes every element with the same ordered sums as the whole-slot form, so both give the
+    same bits on every replica — and fp64 stays per-coordinate on the oracle."""
+    n = groups * per_group
+    if n_gpus < n:
+        pytest.skip(f"needs {n} GPUs")
+    on = _spawn(n, dtype, groups, "train", env={"LSGD_B200_SLICED_GLOBAL": "1"})
+    off = _spawn(n, dtype, groups, "train", env={"LSGD_B200_SLICED_GLOBAL": "0"})
+    for q in range(n):
+        assert np.array_equal(on[q].view(np.uint64), off[q].view(np.uint64)), q
+        assert np.array_equal(on[q].view(np.uint64), on[0].view(np.uint64)), q
+    if dtype == "fp64":
+        from oracle import Oracle, TrainSpec
+        cfg = _cfg(dtype, n, groups)
+        spec = TrainSpec(**{k: getattr(cfg, k) for k in TrainSpec.__dataclass_fields__ if hasattr(cfg, k)})
+        ref = Oracle("port").run_train(spec)["final_params"]
+        rel = np.abs(on[0] - ref) / np.maximum(np.abs(ref), 1e-8)
+        assert rel.max() <= 1e-8, rel.max()
