@@ -66,6 +66,7 @@ class EpochSampler {
 struct RunSpec {
   lsgd_b200_config c{};
   std::vector<int32_t> layers;
+  bool track_versions = false;  // run_train asked for version_at_compute (measured on the device)
   explicit RunSpec(const lsgd_b200_config& cfg);
   int N() const { return c.n_workers; }
   int G() const { return c.algorithm == LSGD_B200_LSGD ? c.n_groups : 1; }

@@ -1084,8 +1084,8 @@ class RankImpl final : public Rank {
   // Measured version_at_compute: on for recorded runs of bounded length (run_train with history / phases), off
   // for the bench and the open-ended rank API (two 1-thread kernels per bucket and layer per step).
   bool track_versions() const {
-    return !synth_ && (hist_rows_ > 0 || spec_.c.record_phases) && spec_.iterations() <= (1 << 20) &&
-           !fused_update();
+    return !synth_ && (hist_rows_ > 0 || spec_.c.record_phases || spec_.track_versions) &&
+           spec_.iterations() <= (1 << 20) && !fused_update();
   }
   void note_version(Worker& w, int b, int64_t rounds, cudaStream_t st) {
     if (w.ver) launch_store_u64(w.ver + b, static_cast<unsigned long long>(rounds), st, lc_);
@@ -1346,8 +1346,20 @@ class RankImpl final : public Rank {
       if (q != skip) fl.f[n++] = w.flags + first + q;
     if (n) launch_wait_flags(fl, n, target, timeout_ns(), timed_out_dev_, st, lc_, max_lead);
   }
+  // Transport conformance under jitter (test_transport.cpp:135-269, the reference's jitter cases): with
+  // LSGD_B200_JITTER_US = J every rank delays each bucket's exchange by a pseudo-random 0..J us (seeded by rank,
+  // step and bucket) on its comm stream, so peers arrive at every flag in varying orders; results must not change.
+  void exchange_jitter(int b, int64_t t, cudaStream_t st) {
+    static const double j_us = std::getenv("LSGD_B200_JITTER_US") ? std::atof(std::getenv("LSGD_B200_JITTER_US")) : 0;
+    if (j_us <= 0) return;
+    SplitMix64 r(0x5eedull + static_cast<uint64_t>(workers_[0]) * 1000003ull + static_cast<uint64_t>(t) * 131ull +
+                 static_cast<uint64_t>(b));
+    launch_sleep(1e-6 * j_us * static_cast<double>(r.u64() % 1024) / 1023.0, st, lc_);
+  }
+
   void exchange_push_bucket(Worker& w, int b, int64_t t, cudaStream_t st) {
     tag_ = b;
+    exchange_jitter(b, t, st);
     const Bucket& bk = geo_.buckets[static_cast<size_t>(b)];
     const int par = static_cast<int>(t & 1);
     const unsigned long long round = static_cast<unsigned long long>(t + 1);

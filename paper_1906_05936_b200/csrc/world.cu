@@ -85,9 +85,11 @@ void run_world(const RunSpec& spec, bool want_history, bool want_workers, TrainO
   // contiguous worker blocks per device (worker i -> GPU i when ndev == N)
   std::vector<std::vector<int>> blocks(static_cast<size_t>(ndev));
   for (int i = 0; i < N; ++i) blocks[static_cast<size_t>(static_cast<int64_t>(i) * ndev / N)].push_back(i);
+  RunSpec rspec = spec;  // outlives the ranks (cleared below)
+  rspec.track_versions = want_workers;
   std::vector<std::unique_ptr<Rank>> ranks;
   for (int r = 0; r < ndev; ++r)
-    ranks.push_back(make_rank(spec, r, blocks[static_cast<size_t>(r)], r == 0 && want_history ? T + 1 : 0));
+    ranks.push_back(make_rank(rspec, r, blocks[static_cast<size_t>(r)], r == 0 && want_history ? T + 1 : 0));
 
   for (int a = 0; a < ndev; ++a) {
     LSGD_CUDA(cudaSetDevice(a));

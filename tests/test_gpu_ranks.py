@@ -230,3 +230,18 @@ def test_sliced_global_is_bitwise_the_whole_slot_form(groups, per_group, dtype, 
         ref = Oracle("port").run_train(spec)["final_params"]
         rel = np.abs(on[0] - ref) / np.maximum(np.abs(ref), 1e-8)
         assert rel.max() <= 1e-8, rel.max()
+
+
+@pytest.mark.parametrize("groups,per_group,dtype", [(2, 2, "fp32"), (4, 1, "fp64"), (1, 4, "fp64"), (2, 1, "fp64")])
+def test_push_exchange_is_deterministic_under_jitter(groups, per_group, dtype, n_gpus):
+    """Transport conformance on the real NVLink kernels (test_transport.cpp:135-269 jitter cases): every rank
+    delays each bucket's exchange by a pseudo-random 0..2000 us (LSGD_B200_JITTER_US), so flags are reached in
+    varying orders across GPUs; the iterates are bitwise those of the undelayed run on every replica (and fp64 stays
+    per-coordinate on the oracle)."""
+    n = groups * per_group
+    if n_gpus < n:
+        pytest.skip(f"needs {n} GPUs")
+    calm = _spawn(n, dtype, groups, "train")
+    jit = _spawn(n, dtype, groups, "train", env={"LSGD_B200_JITTER_US": "2000"})
+    for q in range(n):
+        assert np.array_equal(jit[q].view(np.uint64), calm[q].view(np.uint64)), q
