@@ -1079,6 +1079,92 @@ class RankImpl final : public Rank {
     if (e) return std::strcmp(e, "reverse") == 0;
     return k_ >= 2;
   }
+  // The backward as a sequence of ops: dX_k (x), or the weight-gradient GEMM block(s) of layer k (w; `blk` >= 0:
+  // only the blk-th GEMM block of the layer). Default: reverse (w_{D-1}, x_{D-1}, ..., x_1, w_0) or dX-first
+  // (x_{D-1} .. x_1, w_0 .. w_{D-1}) per bwd_reverse(). LSGD_B200_BWD_SEQ overrides with an explicit list such as
+  // "x2,w1.0,x1,w0,w1.1,w2" (any order with dX_{k+1} before x_k / w_k, every block exactly once): which gradient is
+  // ready when decides which exchange chains hide under the remaining GEMMs. Same kernels, same arithmetic.
+  struct BwdOp {
+    bool dx;
+    int layer;
+    std::vector<int> buckets;  // w: the buckets of the op's GEMM blocks, in row order
+  };
+  std::vector<std::vector<int>> layer_blocks(int k) const {  // buckets grouped by weight-gradient GEMM block
+    std::vector<std::vector<int>> out;
+    for (int b : geo_.layer_buckets[static_cast<size_t>(k)]) {
+      if (geo_.buckets[static_cast<size_t>(b)].blk_rows > 0 || out.empty()) out.emplace_back();
+      out.back().push_back(b);
+    }
+    return out;
+  }
+  std::vector<BwdOp> bwd_seq() const {
+    const int D = synth_ ? 1 : L_.depth();
+    std::vector<BwdOp> seq;
+    auto all_w = [&](int k) {
+      BwdOp op{false, k, {}};
+      for (int b : geo_.layer_buckets[static_cast<size_t>(k)]) op.buckets.push_back(b);
+      return op;
+    };
+    static const char* e = std::getenv("LSGD_B200_BWD_SEQ");
+    if (e && *e && !fused_update() && !synth_) {
+      std::vector<int> seen_x(static_cast<size_t>(D), 0), blk_done;
+      std::string spec(e);
+      size_t pos = 0;
+      int nblk = 0;
+      std::vector<std::vector<std::vector<int>>> blocks(static_cast<size_t>(D));
+      for (int k = 0; k < D; ++k) {
+        blocks[static_cast<size_t>(k)] = layer_blocks(k);
+        nblk += static_cast<int>(blocks[static_cast<size_t>(k)].size());
+      }
+      std::vector<std::vector<int>> used(static_cast<size_t>(D));
+      for (int k = 0; k < D; ++k) used[static_cast<size_t>(k)].assign(blocks[static_cast<size_t>(k)].size(), 0);
+      int done = 0;
+      while (pos <= spec.size()) {
+        size_t end = spec.find(',', pos);
+        if (end == std::string::npos) end = spec.size();
+        const std::string tok = spec.substr(pos, end - pos);
+        pos = end + 1;
+        if (tok.empty()) continue;
+        check<ConfigError>(tok[0] == 'x' || tok[0] == 'w', "LSGD_B200_BWD_SEQ: bad op '", tok, "'");
+        const size_t dot = tok.find('.');
+        const int k = std::atoi(tok.substr(1, dot == std::string::npos ? std::string::npos : dot - 1).c_str());
+        check<ConfigError>(k >= 0 && k < D, "LSGD_B200_BWD_SEQ: layer out of range in '", tok, "'");
+        // delta_k exists once dX_{k+1} ran (delta_{D-1} comes from the head)
+        check<ConfigError>(k == D - 1 || seen_x[static_cast<size_t>(k + 1)], "LSGD_B200_BWD_SEQ: '", tok,
+                           "' before x", k + 1);
+        if (tok[0] == 'x') {
+          check<ConfigError>(k >= 1 && !seen_x[static_cast<size_t>(k)], "LSGD_B200_BWD_SEQ: bad or repeated '", tok,
+                             "'");
+          seen_x[static_cast<size_t>(k)] = 1;
+          seq.push_back(BwdOp{true, k, {}});
+          continue;
+        }
+        auto& bl = blocks[static_cast<size_t>(k)];
+        for (size_t i = 0; i < bl.size(); ++i) {
+          if (dot != std::string::npos && static_cast<size_t>(std::atoi(tok.c_str() + dot + 1)) != i) continue;
+          check<ConfigError>(!used[static_cast<size_t>(k)][i], "LSGD_B200_BWD_SEQ: block ", i, " of layer ", k,
+                             " twice");
+          used[static_cast<size_t>(k)][i] = 1;
+          ++done;
+          seq.push_back(BwdOp{false, k, bl[i]});
+        }
+      }
+      check<ConfigError>(done == nblk, "LSGD_B200_BWD_SEQ: every weight-gradient block exactly once (", done, " of ",
+                         nblk, ")");
+      for (int k = 1; k < D; ++k) check<ConfigError>(seen_x[static_cast<size_t>(k)], "LSGD_B200_BWD_SEQ: x", k, " missing");
+      return seq;
+    }
+    if (bwd_reverse()) {
+      for (int k = D - 1; k >= 0; --k) {
+        seq.push_back(all_w(k));
+        if (k >= 1) seq.push_back(BwdOp{true, k, {}});
+      }
+    } else {
+      for (int k = D - 1; k >= 1; --k) seq.push_back(BwdOp{true, k, {}});
+      for (int k = 0; k < D; ++k) seq.push_back(all_w(k));
+    }
+    return seq;
+  }
   // One worker, one group (N = 1): the gradient is final when produced, so the update runs in the producers'
   // epilogues (dW GEMM, bias) and the separate update pass over g disappears.
   // Measured version_at_compute: on for recorded runs of bounded length (run_train with history / phases), off
@@ -1672,35 +1758,19 @@ class RankImpl final : public Rank {
       head(w);
       // Backward order (bwd_order()): which weight gradient is ready first decides which exchange chains hide
       // under the remaining backward and the next forward. Same kernels, same arithmetic; only the order differs.
-      auto dw_layer = [&](int k) {
-        for (int b : LB[static_cast<size_t>(k)]) {
-          if (!synth_) backward_bucket(w, b);  // row block of dW_k (+ db_k): ready for the exchange right away
+      const std::vector<BwdOp> seq = bwd_seq();
+      if (eager) LSGD_CUDA(cudaEventRecord(ev_dx_[0], main_));  // W_0 is not read by the backward
+      for (const BwdOp& op : seq) {
+        if (op.dx) {
+          if (!synth_) backward_input(w, op.layer);
+          if (eager) LSGD_CUDA(cudaEventRecord(ev_dx_[op.layer], main_));  // W_k is no longer read
+          continue;
+        }
+        for (int b : op.buckets) {  // row block(s) of dW_k (+ db_k): ready for the exchange right away
+          if (!synth_) backward_bucket(w, b);
           if (exchange && !split_) signal(w, kFlagGrad, b, static_cast<unsigned long long>(t + 1), main_);
           if (split_) LSGD_CUDA(cudaEventRecord(ev_bucket_[b], main_));
         }
-      };
-      if (bwd_reverse()) {
-        // reverse layer order: dW_k as soon as delta_k exists (dW_{D-1}, dX_{D-1}, dW_{D-2}, ..., dX_1, dW_0), so
-        // the wide middle layers' exchange chains run under the rest of the backward and the next forward; only
-        // layer 0's chain (the first thing the next forward needs) stays exposed
-        if (eager) LSGD_CUDA(cudaEventRecord(ev_dx_[0], main_));  // W_0 is not read by the backward
-        for (int k = D - 1; k >= 0; --k) {
-          dw_layer(k);
-          if (k >= 1) {
-            if (!synth_) backward_input(w, k);
-            if (eager) LSGD_CUDA(cudaEventRecord(ev_dx_[k], main_));  // W_k is no longer read
-          }
-        }
-      } else {
-        // all input gradients first (dX_{D-1} .. dX_1: the delta chain), then the weight gradients from layer 0
-        // upwards: layer 0's gradient — the first parameters the next forward needs — is ready first, so its
-        // exchange and update run under the remaining dW GEMMs
-        for (int k = D - 1; k >= 1; --k) {
-          if (!synth_) backward_input(w, k);
-        }
-        if (eager)
-          for (int k = 0; k < D; ++k) LSGD_CUDA(cudaEventRecord(ev_dx_[k], main_));  // no W_k is read any more
-        for (int k = 0; k < D; ++k) dw_layer(k);
       }
       phase_mark(widx(w), t, 1, 1, main_);
     }
@@ -1712,10 +1782,8 @@ class RankImpl final : public Rank {
 
     // exchange order: the order buckets finish in the backward (row blocks ascending within a layer)
     std::vector<int> order;
-    for (int i = 0; i < D; ++i) {
-      const int k = bwd_reverse() ? D - 1 - i : i;
-      for (int b : LB[static_cast<size_t>(k)]) order.push_back(b);
-    }
+    for (const BwdOp& op : bwd_seq())
+      for (int b : op.buckets) order.push_back(b);
 
     // communicator work: per bucket, on the comm stream (overlapping the rest of the backward)
     current_phase() = "local_reduce";
@@ -1795,10 +1863,10 @@ class RankImpl final : public Rank {
     } else if (eager) {
       Worker& w = ws_[0];
       current_phase() = "broadcast";
-      for (int i = 0; i < D; ++i) {  // in the order the gradients are produced (see bwd_reverse)
-        const int k = bwd_reverse() ? D - 1 - i : i;
+      for (int b : order) {  // in the order the gradients are produced (bwd_seq)
+        const int k = geo_.buckets[static_cast<size_t>(b)].layer;
         LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_dx_[k], 0));  // W_k is no longer read by this step
-        for (int b : LB[static_cast<size_t>(k)]) {
+        {
           if (reduce_folded()) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_bucket_[b], 0));
           if (flat_nccl()) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_gupd_[b], 0));  // the bucket's allreduce
           if (reduce_folded() && bias_side_[b]) LSGD_CUDA(cudaStreamWaitEvent(upd_, ev_bias_[b], 0));

@@ -245,3 +245,16 @@ def test_push_exchange_is_deterministic_under_jitter(groups, per_group, dtype, n
     jit = _spawn(n, dtype, groups, "train", env={"LSGD_B200_JITTER_US": "2000"})
     for q in range(n):
         assert np.array_equal(jit[q].view(np.uint64), calm[q].view(np.uint64)), q
+
+
+@pytest.mark.parametrize("groups,per_group", [(2, 1), (2, 2)])
+def test_backward_order_changes_no_bits(groups, per_group, n_gpus):
+    """LSGD_B200_BWD_SEQ reorders the backward's dX / dW GEMMs (and with them the exchange and update order): the
+    same kernels on the same data, so every order gives the same bits (256-512-256: x1 = dX_1, w0 / w1 = dW)."""
+    n = groups * per_group
+    if n_gpus < n:
+        pytest.skip(f"needs {n} GPUs")
+    a = _spawn(n, "fp32", groups, "train", env={"LSGD_B200_BWD_SEQ": "w1,x1,w0"})
+    b = _spawn(n, "fp32", groups, "train", env={"LSGD_B200_BWD_SEQ": "x1,w0,w1"})
+    for q in range(n):
+        assert np.array_equal(a[q].view(np.uint64), b[q].view(np.uint64)), q
