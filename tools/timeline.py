@@ -20,6 +20,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--rows", action="store_true", help="e2e path: pinned host rows (step_rows) + async loss D2H")
+    ap.add_argument("--all-ranks", action="store_true", help="also write gpurun_out/timeline_rank<r>.txt per rank")
+    ap.add_argument("--groups", type=int, default=None)
     args = ap.parse_args()
     import torch
 
@@ -42,7 +44,7 @@ def main():
         pg.all_gather_object(out, o)
         return out
 
-    cfg = bench.workload(args.workload, world, None, args.algo, args.global_allreduce)
+    cfg = bench.workload(args.workload, world, None, args.algo, args.global_allreduce, args.groups)
     r = Rank(cfg, rank, local)
     if rank == 0:
         print("# buckets (id: layer rows n):", ", ".join(f"{i}: L{b[0]} {b[1]} {b[2]}" for i, b in enumerate(r.buckets()))
@@ -76,6 +78,11 @@ def main():
     buf = C.create_string_buffer(1 << 20)
     N.check(fn(r.h, buf, len(buf)))
     lines = [ln.split("\t") for ln in buf.value.decode().strip().splitlines()]
+    if args.all_ranks:  # every rank's timeline (origin: each rank's timing(True) right after a host barrier)
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        with open(os.path.join(ROOT, "gpurun_out", f"timeline_rank{rank}.txt"), "w") as f:
+            for fam, a, b, tag in lines:
+                f.write(f"{fam:10s} {tag:>4s} {float(a):9.3f} {float(b):9.3f} {1e3 * (float(b) - float(a)):8.1f} us\n")
     if rank == 0:
         tot = {}
         for fam, a, b, tag in lines:  # tag: bucket id, 100 + k forward / 200 + k dX GEMM of layer k
