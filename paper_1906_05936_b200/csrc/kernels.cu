@@ -820,7 +820,12 @@ void launch_global_update(const GlobalUpdateArgs<T>& a, bool exact, cudaStream_t
   check<Error>(aligned, "global_update: slices must be 16-byte aligned vectors");
   const bool vec_params = (reinterpret_cast<uintptr_t>(a.w + a.first) & 15u) == 0 &&
                           (a.v == nullptr || (reinterpret_cast<uintptr_t>(a.v + a.first) & 15u) == 0);
-  const int g = grid_for(a.len / Vec<T>::kN + 1, 256, 148 * 8);
+  static const int cap = [] {  // LSGD_B200_GLOBAL_CTAS (A/B knob)
+    const char* e = std::getenv("LSGD_B200_GLOBAL_CTAS");
+    const int v = e ? std::atoi(e) : 148 * 8;
+    return v > 0 ? v : 148 * 8;
+  }();
+  const int g = grid_for(a.len / Vec<T>::kN + 1, 256, cap);
   if (exact) global_update_kernel<T, true><<<g, 256, side_smem(), st>>>(a, vec_params);
   else global_update_kernel<T, false><<<g, 256, side_smem(), st>>>(a, vec_params);
   ++lc.n;
