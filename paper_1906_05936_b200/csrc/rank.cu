@@ -1345,6 +1345,14 @@ class RankImpl final : public Rank {
     if (e) return std::atoi(e) != 0;
     return G_ > 2;
   }
+  // Members pull the slot owners' averages straight into their update (NVLink loads from the owner's gbar) instead
+  // of the owner pushing them into every member's gfull: no gfull write + read (8 B per parameter on (k-1)/k of P)
+  // and no remote stores in the owner's global kernel. Whole-slot form only (k >= 2). LSGD_B200_PULL_AVG = 0 / 1.
+  bool pull_avg() const {
+    static const char* e = std::getenv("LSGD_B200_PULL_AVG");
+    if (k_ < 2 || !own_slot_fused() || sliced_global()) return false;
+    return e ? std::atoi(e) != 0 : false;
+  }
   int64_t piece_len(const Bucket& bk) const {  // elements of each of the G pieces of a slot (64-aligned)
     return sliced_global() ? round_up((bk.S + G_ - 1) / G_, kAlign) : bk.S;
   }
@@ -1583,6 +1591,10 @@ class RankImpl final : public Rank {
           ga.w_lo = w.tc.w_lo + bk.pstart;
         }
       }
+      if (pull_avg()) {  // the members read the average from this owner's gbar after the arrival flag
+        ga.n_push = 0;
+        ga.out_local = w.gbar + bk.goff + p0;
+      }
       DstList<T> remote = ga.push;
       const int n_remote = ga.n_push;
       const bool fan_dma = dma(8) && n_remote > 0;
@@ -1597,7 +1609,15 @@ class RankImpl final : public Rank {
       if (fan_dma && plen > 0)
         for (int q = 0; q < n_remote; ++q)
           LSGD_CUDA(cudaMemcpyAsync(remote.p[q], ga.out_local, sizeof(T) * plen, cudaMemcpyDeviceToDevice, st));
-      if (n_remote) launch_signal_many(others, n_remote, round, st, lc_);
+      if (pull_avg()) {
+        int nm = 0;
+        SignalList mem{};
+        for (int d = 0; d < N_; ++d)
+          if (d != w.id && d / k_ == w.g) mem.f[nm++] = peer_arrived(d, b, arr);
+        if (nm) launch_signal_many(mem, nm, round, st, lc_);
+      } else if (n_remote) {
+        launch_signal_many(others, n_remote, round, st, lc_);
+      }
       LSGD_CUDA(cudaEventRecord(ev_gupd_[b], st));
       return;
     }
@@ -1668,6 +1688,11 @@ class RankImpl final : public Rank {
       }
       a.slices.p[0] = w.gfull + bk.poff;
       a.slice_len = bk.S * k_;
+      if (pull_avg()) {  // slot j's average straight from its owner's gbar over NVLink (own slot: skipped below)
+        const auto mem = group_members(w.g);
+        for (int j = 0; j < k_; ++j) a.slices.p[j] = peer_gbar(mem[static_cast<size_t>(j)]) + bk.goff;
+        a.slice_len = bk.S;
+      }
       if (own) {
         a.skip_lo = static_cast<int64_t>(w.j) * bk.S + p0;
         a.skip_hi = a.skip_lo + plen;

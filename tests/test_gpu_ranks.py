@@ -258,3 +258,22 @@ def test_backward_order_changes_no_bits(groups, per_group, n_gpus):
     b = _spawn(n, "fp32", groups, "train", env={"LSGD_B200_BWD_SEQ": "x1,w0,w1"})
     for q in range(n):
         assert np.array_equal(a[q].view(np.uint64), b[q].view(np.uint64)), q
+
+
+@pytest.mark.parametrize("groups,per_group,dtype", [(2, 2, "fp32"), (1, 4, "fp64"), (1, 2, "fp32")])
+def test_pulled_averages_are_bitwise_the_pushed_ones(groups, per_group, dtype, n_gpus):
+    """LSGD_B200_PULL_AVG: members read the slot owners' averages over NVLink inside their update instead of having
+    them pushed into gfull first — the same values, so the same bits (and fp64 per-coordinate on the oracle)."""
+    n = groups * per_group
+    if n_gpus < n:
+        pytest.skip(f"needs {n} GPUs")
+    pull = _spawn(n, dtype, groups, "train", env={"LSGD_B200_PULL_AVG": "1"})
+    push = _spawn(n, dtype, groups, "train", env={"LSGD_B200_PULL_AVG": "0"})
+    for q in range(n):
+        assert np.array_equal(pull[q].view(np.uint64), push[q].view(np.uint64)), q
+    if dtype == "fp64":
+        from oracle import Oracle, TrainSpec
+        cfg = _cfg(dtype, n, groups)
+        spec = TrainSpec(**{k: getattr(cfg, k) for k in TrainSpec.__dataclass_fields__ if hasattr(cfg, k)})
+        ref = Oracle("port").run_train(spec)["final_params"]
+        assert (np.abs(pull[0] - ref) / np.maximum(np.abs(ref), 1e-8)).max() <= 1e-8
