@@ -86,7 +86,7 @@ Geometry::Geometry(const RunSpec& spec, int es) : esize(es) {
     Layout L(spec.layers);
     P = L.n_params;
     check<ConfigError>(L.depth() <= kMaxBuckets, "at most ", kMaxBuckets, " layers are supported");
-    // Exchange buckets are row blocks of W_k (heights a multiple of the 128-row GEMM tile): 16M parameters on one
+    // Exchange buckets are row blocks of W_k (heights a multiple of the 128-row GEMM tile): 64M parameters on one
     // GPU, 32M with an exchange. The weight-gradient GEMM runs over blocks of consecutive buckets: one bucket per
     // block for one worker per group (2x1: 560k samples/s vs 539k with 64M blocks, 499k with 64M buckets), 64M
     // blocks for groups of k >= 2, whose exchange is a scatter + reduce + global chain per bucket: 32M buckets in
@@ -97,7 +97,9 @@ Geometry::Geometry(const RunSpec& spec, int es) : esize(es) {
     const char* env = std::getenv("LSGD_B200_BUCKET_ELEMS");
     const char* genv = std::getenv("LSGD_B200_GEMM_ELEMS");
     const double kMi = 1024.0 * 1024.0;
-    const double kBucketElems = env ? std::max(1.0, std::atof(env)) : (spec.N() > 1 ? 32.0 : 16.0) * kMi;
+    // N = 1: 64M (layer 1 in two blocks): fewer, larger weight-gradient GEMMs overlapped by fewer update launches
+    // (A/B, 3 rounds on one box: 345-350k samples/s vs 337-339k with 16M; profiles/r2_n1_bucket_ab.log)
+    const double kBucketElems = env ? std::max(1.0, std::atof(env)) : (spec.N() > 1 ? 32.0 : 64.0) * kMi;
     const double kGemmElems = std::max(kBucketElems, genv ? std::atof(genv) : (kk >= 2 ? 64.0 * kMi : 0.0));
     layer_buckets.resize(static_cast<size_t>(L.depth()));
     // Layer 0's gradient is the first one the backward produces and the first one the next forward needs: with an
