@@ -301,6 +301,9 @@ class RankImpl final : public Rank {
     for (int b = 0; b < kMaxBuckets; ++b) cudaEventDestroy(ev_dx_[b]);
     for (int b = 0; b < kMaxBuckets; ++b) cudaEventDestroy(ev_gupd_[b]);
     cudaEventDestroy(join_ev_);
+    if (iod_) cudaStreamDestroy(iod_);
+    if (ev_pre_exch_) cudaEventDestroy(ev_pre_exch_);
+    if (ev_io_done_) cudaEventDestroy(ev_io_done_);
     if (base_ev_) cudaEventDestroy(base_ev_);
     if (io_) {
       cudaStreamDestroy(io_);
@@ -1001,10 +1004,31 @@ class RankImpl final : public Rank {
     } else {
       std::memcpy(dst, src, sizeof(int32_t) * B_ * ws_.size());
     }
+    // Injected io latency (executors.hpp:213-216). Emulated ranks (several workers on one stream) model the
+    // reference's concurrent rank threads: one sleep per step for all of them, and under LSGD on a side stream
+    // forked before the previous round's exchange, so io(t) overlaps the communicators' global allreduce(t-1)
+    // (and its injected link delay) as the reference's worker and communicator threads do (executors.cpp:210-229).
+    const bool emu_delay = ws_.size() > 1 && spec_.c.io_delay_s > 0;
+    if (emu_delay && alg_ == LSGD_B200_LSGD) {
+      if (!iod_) {
+        LSGD_CUDA(cudaStreamCreateWithFlags(&iod_, cudaStreamNonBlocking));
+        LSGD_CUDA(cudaEventCreateWithFlags(&ev_io_done_, cudaEventDisableTiming));
+      }
+      if (t > 0) LSGD_CUDA(cudaStreamWaitEvent(iod_, ev_pre_exch_, 0));
+      for (size_t i = 0; i < ws_.size(); ++i) phase_mark(i, t, 0, 0, iod_);
+      launch_sleep(spec_.c.io_delay_s, iod_, lc_);
+      LSGD_CUDA(cudaEventRecord(ev_io_done_, iod_));
+      LSGD_CUDA(cudaStreamWaitEvent(main_, ev_io_done_, 0));
+    } else if (emu_delay) {
+      for (size_t i = 0; i < ws_.size(); ++i) phase_mark(i, t, 0, 0, main_);
+      launch_sleep(spec_.c.io_delay_s, main_, lc_);
+    }
     for (size_t i = 0; i < ws_.size(); ++i) {
       Worker& w = ws_[i];
-      phase_mark(i, t, 0, 0, main_);
-      launch_sleep(spec_.c.io_delay_s, main_, lc_);
+      if (!emu_delay) {
+        phase_mark(i, t, 0, 0, main_);
+        launch_sleep(spec_.c.io_delay_s, main_, lc_);
+      }
       LSGD_CUDA(cudaMemcpyAsync(w.idx, dst + i * B_, sizeof(int32_t) * B_, cudaMemcpyHostToDevice, main_));
       {
         Timed tm(this, "gather", main_);
@@ -1812,6 +1836,10 @@ class RankImpl final : public Rank {
     for (const BwdOp& op : bwd_seq())
       for (int b : op.buckets) order.push_back(b);
 
+    if (iod_) {  // emulated ranks: the next io forks here, ahead of this round's exchange
+      if (!ev_pre_exch_) LSGD_CUDA(cudaEventCreateWithFlags(&ev_pre_exch_, cudaEventDisableTiming));
+      LSGD_CUDA(cudaEventRecord(ev_pre_exch_, main_));
+    }
     // communicator work: per bucket, on the comm stream (overlapping the rest of the backward)
     current_phase() = "local_reduce";
     if (flat_nccl() && split_) {
@@ -1970,6 +1998,8 @@ class RankImpl final : public Rank {
   std::vector<T*> own_x_;
   std::vector<int32_t*> own_y_;  // per layer: dX_k issued (W_k free for its update)
   cudaStream_t upd_ = nullptr;
+  cudaStream_t iod_ = nullptr;  // emulated ranks: the injected io latency, overlapping the previous exchange
+  cudaEvent_t ev_pre_exch_ = nullptr, ev_io_done_ = nullptr;
   std::vector<char*> peer_base_;
   std::vector<char*> ipc_opened_;
   ncclComm_t slice_comm_ = nullptr, flat_comm_ = nullptr;
