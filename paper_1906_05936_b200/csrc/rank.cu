@@ -1364,12 +1364,14 @@ class RankImpl final : public Rank {
 
   // The global stage of the push exchange sliced over the G owners of each slot (reduce-scatter + all-gather, see
   // exchange_push_bucket). LSGD_B200_SLICED_GLOBAL = 0 / 1 forces it; default: on for G > 2, where the whole-slot
-  // form's (G-1) slot lengths of egress per owner dominate.
+  // form's (G-1) slot lengths of egress per owner dominate (4x1: 888k vs 459k samples/s), and for one worker per
+  // group, where every GPU would otherwise sum and update all P parameters (2x1: 591-593k vs 562k); off for 2 x k
+  // with k >= 2 (2x2: 1.000M vs 936k). profiles/r2_layouts_n4_*.log, r2_n2_ab.log.
   bool sliced_global() const {
     static const char* e = std::getenv("LSGD_B200_SLICED_GLOBAL");
     if (G_ <= 1 || !own_slot_fused() || N_ > kMaxPeers) return false;  // one arrived word per source owner
     if (e) return std::atoi(e) != 0;
-    return G_ > 2;
+    return G_ > 2 || k_ == 1;
   }
   // Members pull the slot owners' averages straight into their update (NVLink loads from the owner's gbar) instead
   // of the owner pushing them into every member's gfull: no gfull write + read (8 B per parameter on (k-1)/k of P)
