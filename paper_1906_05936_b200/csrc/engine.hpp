@@ -69,6 +69,12 @@ struct Bucket {
   bool blk_bias = false;
 };
 
+// Direct two-hop exchange for groups of k >= 2 and G >= 2 (LSGD_B200_DIRECT=1): every member's sub-slice j goes by
+// copy engine straight to the slot-j owner of EVERY group; owners sum all N sub-slices in the reference's order
+// (groups ascending, members ascending within a group, + 0.0, / N per group) — no owner reduce kernel, no group-sum
+// hop. Stage holds one sub-slice per source GPU, double-buffered by round parity.
+bool direct_exchange(const RunSpec& spec);
+
 struct Geometry {
   int64_t P = 0, Ppad = 0, Sg = 0;  // params, padded payload, per-slot slice elements (sum of bucket S)
   int esize = 4;

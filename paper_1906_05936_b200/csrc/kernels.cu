@@ -551,18 +551,23 @@ __global__ void __launch_bounds__(256) global_update_kernel(const __grid_constan
   bool bad = false;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nvec; i += stride) {
     const int64_t e = i * V;
-    Vec<T> s = ld16(a.src.p[0] + e);  // this group's slot sum, recomputed (K6 order)
-    for (int m = 1; m < a.k; ++m) {
-      const Vec<T> x = ld16(a.src.p[m] + e);
+    auto member_sum = [&](int base) {  // a group's slot sum from its k member sub-slices (K6 order, + 0.0, / N)
+      Vec<T> s = ld16(a.src.p[base] + e);
+      for (int m = 1; m < a.k; ++m) {
+        const Vec<T> x = ld16(a.src.p[base + m] + e);
 #pragma unroll
-      for (int q = 0; q < V; ++q) s.v[q] = Rn<T>::add(s.v[q], x.v[q]);
-    }
+        for (int q = 0; q < V; ++q) s.v[q] = Rn<T>::add(s.v[q], x.v[q]);
+      }
 #pragma unroll
-    for (int q = 0; q < V; ++q) {
-      if (a.add_zero) s.v[q] = Rn<T>::add(s.v[q], T(0));
-      if (a.divisor != T(0)) s.v[q] = Rn<T>::div(s.v[q], a.divisor);
-    }
+      for (int q = 0; q < V; ++q) {
+        if (a.add_zero) s.v[q] = Rn<T>::add(s.v[q], T(0));
+        if (a.divisor != T(0)) s.v[q] = Rn<T>::div(s.v[q], a.divisor);
+      }
+      return s;
+    };
+    const Vec<T> s = member_sum(a.direct ? a.g * a.k : 0);  // this group's slot sum, recomputed
     auto group_sum = [&](int gg) {  // the other groups' K6 results (recomputed from raw payloads when k = 1)
+      if (a.direct) return member_sum(gg * a.k);
       Vec<T> x = ld16(a.gsum.p[gg] + e);
       if (a.gsum_raw) {
 #pragma unroll
@@ -812,8 +817,9 @@ void launch_copy_pairs(SrcList<T> src, DstList<T> dst, int n_pairs, int64_t len,
 template <typename T>
 void launch_global_update(const GlobalUpdateArgs<T>& a, bool exact, cudaStream_t st, LaunchCounter& lc) {
   bool aligned = a.len % Vec<T>::kN == 0;
-  for (int i = 0; i < a.k; ++i) aligned = aligned && (reinterpret_cast<uintptr_t>(a.src.p[i]) & 15u) == 0;
-  for (int g = 0; g < a.G; ++g)
+  const int n_src = a.direct ? a.k * a.G : a.k;
+  for (int i = 0; i < n_src; ++i) aligned = aligned && (reinterpret_cast<uintptr_t>(a.src.p[i]) & 15u) == 0;
+  for (int g = 0; g < a.G && !a.direct; ++g)
     if (g != a.g) aligned = aligned && (reinterpret_cast<uintptr_t>(a.gsum.p[g]) & 15u) == 0;
   for (int d = 0; d < a.n_push; ++d) aligned = aligned && (reinterpret_cast<uintptr_t>(a.push.p[d]) & 15u) == 0;
   if (a.out_local) aligned = aligned && (reinterpret_cast<uintptr_t>(a.out_local) & 15u) == 0;

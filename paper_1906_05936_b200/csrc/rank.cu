@@ -76,6 +76,13 @@ struct PhaseEvents {
 };
 }  // namespace
 
+bool direct_exchange(const RunSpec& spec) {
+  static const char* e = std::getenv("LSGD_B200_DIRECT");
+  return e && std::atoi(e) != 0 && spec.c.algorithm == LSGD_B200_LSGD && spec.G() > 1 && spec.k() > 1 &&
+         spec.c.global_algo == LSGD_B200_GLOBAL_ORDERED && spec.c.model == LSGD_B200_MODEL_MLP &&
+         spec.N() <= kMaxPeers;
+}
+
 Geometry::Geometry(const RunSpec& spec, int es) : esize(es) {
   if (spec.c.model == LSGD_B200_MODEL_SYNTHETIC_GRADIENT) {
     P = spec.c.synthetic_params;
@@ -164,7 +171,9 @@ Geometry::Geometry(const RunSpec& spec, int es) : esize(es) {
   peer.gfull = round_up(peer.gbar + Sg * es, 256);
   peer.stage = round_up(peer.gfull + Ppad * es, 256);
   const int G = spec.G();
-  const int64_t stage_elems = k > 1 ? k * Sg : 0, gstage_elems = G > 1 ? G * Sg : 0;  // only what the layout uses
+  const bool direct = direct_exchange(spec);
+  const int64_t stage_elems = direct ? 2 * spec.N() * Sg : (k > 1 ? k * Sg : 0);
+  const int64_t gstage_elems = (G > 1 && !direct) ? G * Sg : 0;  // only what the layout uses
   peer.gstage[0] = round_up(peer.stage + stage_elems * es, 256);
   peer.gstage[1] = round_up(peer.gstage[0] + gstage_elems * es, 256);
   peer.total = round_up(peer.gstage[1] + gstage_elems * es, 256);
@@ -242,6 +251,7 @@ class RankImpl final : public Rank {
     }
     use_tc_ = tc_eligible();
     for (int wid : workers_) alloc_worker(wid);
+    direct_ = direct_exchange(spec_) && split_;
     if (hist_rows_ > 0)
       LSGD_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hist_), sizeof(T) * hist_rows_ * geo_.P, cudaHostAllocDefault));
     LSGD_CUDA(cudaStreamSynchronize(main_));  // zeroed flags/payloads are in place before any peer connects
@@ -1074,7 +1084,7 @@ class RankImpl final : public Rank {
   // The push exchange's scatter is fused into the producers (dW epilogue, bias, loss) on the tensor-core path.
   bool fused_scatter() const {
     const bool exchange = !flat_nccl() && !reduce_folded() && alg_ != LSGD_B200_SEQUENTIAL;
-    return exchange && split_ && use_tc_ && k_ > 1 && !dma(2);
+    return exchange && split_ && use_tc_ && k_ > 1 && !dma(2) && !direct_;
   }
   // Push exchange (one worker per GPU, ordered global sum): the owner's K7 + broadcast + K8 for its own slot run as
   // one kernel on the comm stream; apply_bucket then updates the other members' slots only.
@@ -1369,7 +1379,7 @@ class RankImpl final : public Rank {
   // with k >= 2 (2x2: 1.000M vs 936k). profiles/r2_layouts_n4_*.log, r2_n2_ab.log.
   bool sliced_global() const {
     static const char* e = std::getenv("LSGD_B200_SLICED_GLOBAL");
-    if (G_ <= 1 || !own_slot_fused() || N_ > kMaxPeers) return false;  // one arrived word per source owner
+    if (G_ <= 1 || !own_slot_fused() || N_ > kMaxPeers || direct_) return false;  // one arrived word per source
     if (e) return std::atoi(e) != 0;
     return G_ > 2 || k_ == 1;
   }
@@ -1378,7 +1388,7 @@ class RankImpl final : public Rank {
   // and no remote stores in the owner's global kernel. Whole-slot form only (k >= 2). LSGD_B200_PULL_AVG = 0 / 1.
   bool pull_avg() const {
     static const char* e = std::getenv("LSGD_B200_PULL_AVG");
-    if (k_ < 2 || !own_slot_fused() || sliced_global()) return false;
+    if (k_ < 2 || !own_slot_fused() || sliced_global() || direct_) return false;
     return e ? std::atoi(e) != 0 : false;
   }
   int64_t piece_len(const Bucket& bk) const {  // elements of each of the G pieces of a slot (64-aligned)
@@ -1468,6 +1478,78 @@ class RankImpl final : public Rank {
       if (q != skip) fl.f[n++] = w.flags + first + q;
     if (n) launch_wait_flags(fl, n, target, timeout_ns(), timed_out_dev_, st, lc_, max_lead);
   }
+  // Direct two-hop exchange (direct_exchange(), engine.hpp): this GPU's sub-slice j goes by copy engine to the
+  // slot-j owner of every group (stage[par][my id]); the owner of slot `me` then sums all N sub-slices in the
+  // reference's order, updates its slot and pushes the average to its group's members (the broadcast hop).
+  T* peer_stage_direct(int wid, int par, int src) const {
+    return reinterpret_cast<T*>(base(wid) + geo_.peer.stage) +
+           (static_cast<int64_t>(par) * N_ + src) * geo_.Sg;
+  }
+  void exchange_direct_bucket(Worker& w, int b, int64_t t, cudaStream_t st) {
+    const Bucket& bk = geo_.buckets[static_cast<size_t>(b)];
+    const int par = static_cast<int>(t & 1);
+    const unsigned long long round = static_cast<unsigned long long>(t + 1);
+    const int me = w.j;
+    SignalList sl{};
+    int n = 0;
+    {
+      Timed tm(this, "scatter", st);
+      for (int q = 0; q < G_; ++q)
+        for (int j = 0; j < k_; ++j) {
+          const int owner = q * k_ + j;
+          if (owner == w.id) continue;
+          LSGD_CUDA(cudaMemcpyAsync(peer_stage_direct(owner, par, w.id) + bk.goff,
+                                    w.payload + bk.poff + static_cast<int64_t>(j) * bk.S, sizeof(T) * bk.S,
+                                    cudaMemcpyDeviceToDevice, st));
+          sl.f[n++] = peer_flag_word(owner, kStaged + b * kMaxPeers + w.id);
+        }
+    }
+    launch_signal_many(sl, n, round, st, lc_);
+    // every other GPU's sub-slice `me` of round t; a source may already be one round ahead (double-buffered)
+    wait_own(w, kStaged + b * kMaxPeers, N_, w.id, round, st, 1);
+    GlobalUpdateArgs<T> ga;
+    for (int id = 0; id < N_; ++id)
+      ga.src.p[id] = id == w.id ? w.payload + bk.poff + static_cast<int64_t>(me) * bk.S
+                                : peer_stage_direct(w.id, par, id) + bk.goff;
+    ga.direct = true;
+    ga.k = k_;
+    ga.G = G_;
+    ga.g = w.g;
+    ga.add_zero = alg_ == LSGD_B200_LSGD;
+    ga.divisor = static_cast<T>(N_);
+    ga.len = bk.S;
+    SignalList others{};
+    const auto members = group_members(w.g);
+    for (int m = 0; m < k_; ++m) {
+      if (m == me) continue;
+      others.f[ga.n_push] = peer_arrived(members[static_cast<size_t>(m)], b, me);
+      ga.push.p[ga.n_push++] = peer_gfull(members[static_cast<size_t>(m)]) + bk.poff + static_cast<int64_t>(me) * bk.S;
+    }
+    ga.first = static_cast<int64_t>(me) * bk.S;
+    ga.n_params = bk.n;
+    ga.w = w.w + bk.pstart;
+    ga.v = w.v ? w.v + bk.pstart : nullptr;
+    ga.mode = spec_.c.mode;
+    ga.lr = static_cast<T>(spec_.lr(t));
+    ga.momentum = static_cast<T>(spec_.c.momentum);
+    ga.weight_decay = static_cast<T>(spec_.c.weight_decay);
+    ga.loss_out = bk.loss ? w.loss_hist + (t % kLossCap) : nullptr;
+    ga.bad = bad_dev_;
+    if constexpr (std::is_same_v<T, float>) {
+      if (use_tc_ && !w.tc.weights_split_in_smem) {
+        ga.w_hi = w.tc.w_hi + bk.pstart;
+        ga.w_lo = w.tc.w_lo + bk.pstart;
+      }
+    }
+    const int n_remote = ga.n_push;
+    {
+      Timed tm(this, "global", st);
+      launch_global_update<T>(ga, exact_, st, lc_);
+    }
+    if (n_remote) launch_signal_many(others, n_remote, round, st, lc_);
+    LSGD_CUDA(cudaEventRecord(ev_gupd_[b], st));
+  }
+
   // Transport conformance under jitter (test_transport.cpp:135-269, the reference's jitter cases): with
   // LSGD_B200_JITTER_US = J every rank delays each bucket's exchange by a pseudo-random 0..J us (seeded by rank,
   // step and bucket) on its comm stream, so peers arrive at every flag in varying orders; results must not change.
@@ -1487,6 +1569,10 @@ class RankImpl final : public Rank {
     const unsigned long long round = static_cast<unsigned long long>(t + 1);
     const auto members = group_members(w.g);
     const int me = w.j;
+    if (direct_) {
+      exchange_direct_bucket(w, b, t, st);
+      return;
+    }
     if (k_ > 1 && fused_scatter()) {
       wait_own(w, kStaged + b * kMaxPeers, k_, me, round, st, 0);  // the producers already scattered (main stream)
     } else if (k_ > 1) {
@@ -2000,6 +2086,7 @@ class RankImpl final : public Rank {
   std::vector<T*> own_x_;
   std::vector<int32_t*> own_y_;  // per layer: dX_k issued (W_k free for its update)
   cudaStream_t upd_ = nullptr;
+  bool direct_ = false;  // direct two-hop exchange (LSGD_B200_DIRECT)
   cudaStream_t iod_ = nullptr;  // emulated ranks: the injected io latency, overlapping the previous exchange
   cudaEvent_t ev_pre_exch_ = nullptr, ev_io_done_ = nullptr;
   std::vector<char*> peer_base_;

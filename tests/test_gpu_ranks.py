@@ -277,3 +277,22 @@ def test_pulled_averages_are_bitwise_the_pushed_ones(groups, per_group, dtype, n
         spec = TrainSpec(**{k: getattr(cfg, k) for k in TrainSpec.__dataclass_fields__ if hasattr(cfg, k)})
         ref = Oracle("port").run_train(spec)["final_params"]
         assert (np.abs(pull[0] - ref) / np.maximum(np.abs(ref), 1e-8)).max() <= 1e-8
+
+
+@pytest.mark.parametrize("groups,per_group,dtype", [(2, 2, "fp32"), (2, 2, "fp64")])
+def test_direct_exchange_is_bitwise_the_three_hop_form(groups, per_group, dtype, n_gpus):
+    """LSGD_B200_DIRECT: members copy their sub-slices straight to every group's slot owner, which forms all group sums
+    itself (no owner reduce, no group-sum hop) — the same ordered sums, so the same bits; fp64 on the oracle."""
+    n = groups * per_group
+    if n_gpus < n:
+        pytest.skip(f"needs {n} GPUs")
+    d = _spawn(n, dtype, groups, "train", env={"LSGD_B200_DIRECT": "1"})
+    h = _spawn(n, dtype, groups, "train", env={"LSGD_B200_DIRECT": "0"})
+    for q in range(n):
+        assert np.array_equal(d[q].view(np.uint64), h[q].view(np.uint64)), q
+    if dtype == "fp64":
+        from oracle import Oracle, TrainSpec
+        cfg = _cfg(dtype, n, groups)
+        spec = TrainSpec(**{k: getattr(cfg, k) for k in TrainSpec.__dataclass_fields__ if hasattr(cfg, k)})
+        ref = Oracle("port").run_train(spec)["final_params"]
+        assert (np.abs(d[0] - ref) / np.maximum(np.abs(ref), 1e-8)).max() <= 1e-8
