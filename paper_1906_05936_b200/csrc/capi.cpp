@@ -6,12 +6,15 @@
 
 #include <algorithm>
 #include <cstring>
+#include <unistd.h>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
 
 #include "../../include/lsgd_b200.h"
 #include "engine.hpp"
+#include "nvls.hpp"
 #include "host.hpp"
 
 using namespace lsgd_b200;
@@ -38,16 +41,33 @@ int guarded(F&& f) {
 
 constexpr int64_t kIpcBytes = sizeof(cudaIpcMemHandle_t);  // 64
 constexpr int64_t kUidBytes = sizeof(ncclUniqueId);         // 128
-constexpr int64_t kBlobBytes = kIpcBytes + 2 * kUidBytes;
+constexpr int64_t kNvlsOff = kIpcBytes + 2 * kUidBytes;   // group leader: pid, multicast fd, object size
+constexpr int64_t kBlobBytes = kNvlsOff + 16;
 
 }  // namespace
+
+struct lsgd_b200_rank;
+namespace {
+char* leader_block_of(lsgd_b200_rank* r, int leader);
+}
 
 struct lsgd_b200_rank {
   std::unique_ptr<RunSpec> spec;
   std::unique_ptr<Rank> rank;
   int id = 0;
   ncclUniqueId slice_uid{}, flat_uid{};
+  std::map<int, char*> peer_bases;  // IPC-mapped peer blocks (connect)
+  uint64_t nvls_mc = 0;  // group leader: the multicast object created at export (attached at connect)
+  size_t nvls_size = 0;
 };
+
+namespace {
+char* leader_block_of(lsgd_b200_rank* r, int leader) {
+  auto it = r->peer_bases.find(leader);
+  check<Error>(it != r->peer_bases.end(), "NVLS: leader ", leader, "'s block is not mapped");
+  return it->second;
+}
+}  // namespace
 
 extern "C" {
 
@@ -272,6 +292,17 @@ int lsgd_b200_rank_export(lsgd_b200_rank* r, void* blob) {
       LSGD_NCCL(ncclGetUniqueId(&r->flat_uid));
       std::memcpy(b + kIpcBytes + kUidBytes, &r->flat_uid, kUidBytes);
     }
+    if (r->rank->nvls_wanted() && r->id % k == 0 && !r->nvls_mc) {  // group leader: the NVLS multicast object
+      r->nvls_size = nvls_size(r->rank->nvls_bytes(), k);
+      int fd = -1;
+      r->nvls_mc = nvls_create(r->nvls_size, k, &fd);
+      const int32_t pid = static_cast<int32_t>(getpid());
+      const int32_t fd32 = fd;
+      const uint64_t sz = r->nvls_size;
+      std::memcpy(b + kNvlsOff, &pid, 4);
+      std::memcpy(b + kNvlsOff + 4, &fd32, 4);
+      std::memcpy(b + kNvlsOff + 8, &sz, 8);
+    }
   });
 }
 
@@ -288,6 +319,7 @@ int lsgd_b200_rank_connect(lsgd_b200_rank* r, const void* all_blobs) {
       void* p = nullptr;
       LSGD_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
       r->rank->set_peer_base(w, static_cast<char*>(p));
+      r->peer_bases[w] = static_cast<char*>(p);
       note_ipc_mapping(r->rank.get(), static_cast<char*>(p));
     }
     ncclComm_t slice = nullptr, flat = nullptr;
@@ -303,6 +335,19 @@ int lsgd_b200_rank_connect(lsgd_b200_rank* r, const void* all_blobs) {
       flat = static_cast<ncclComm_t>(nccl_init_rank(N, &uid, r->id, init_timeout(s.c.collective_timeout_s)));
     }
     r->rank->set_nccl(slice, flat);
+    if (r->rank->nvls_wanted()) {  // join the group's multicast object (leader's blob: pid, fd, size)
+      const int leader = (r->id / k) * k;
+      const char* lb = all + leader * kBlobBytes + kNvlsOff;
+      int32_t pid = 0, fd = -1;
+      uint64_t sz = 0;
+      std::memcpy(&pid, lb, 4);
+      std::memcpy(&fd, lb + 4, 4);
+      std::memcpy(&sz, lb + 8, 8);
+      check<Error>(sz > 0, "NVLS: the group leader published no multicast object");
+      const uint64_t mc = leader == r->id ? r->nvls_mc : nvls_import(pid, fd);
+      char* lblock = leader == r->id ? r->rank->peer_block(r->id) : leader_block_of(r, leader);
+      r->rank->nvls_join(mc, static_cast<size_t>(sz), lblock, r->id % k, k, init_timeout(s.c.collective_timeout_s));
+    }
     enable_phase_recording(r->rank.get());
   });
 }

@@ -45,7 +45,9 @@ constexpr int kArrived = 3 * kMaxBuckets;
 constexpr int kStaged = kArrived + kMaxBuckets * kMaxPeers;
 // flags[kGsum + b * kMaxPeers + g]: group g's slot sum of bucket b is in this owner's gstage[par][g]
 constexpr int kGsum = kStaged + kMaxBuckets * kMaxPeers;
-constexpr int kFlagWords = kGsum + kMaxBuckets * kMaxPeers;
+// flags[kNvlsAdded + j] (in the group leader's block): member j added its device to the group's multicast object
+constexpr int kNvlsAdded = kGsum + kMaxBuckets * kMaxPeers;
+constexpr int kFlagWords = kNvlsAdded + kMaxPeers;
 
 // Gradient buckets: one per layer (that layer's [W_k | b_k] block, contiguous in the reference's parameter
 // layout, mlp.hpp:14-18), the loss slot riding the last layer's bucket. Each bucket is split into k sub-slices of
@@ -94,6 +96,14 @@ class Rank {
   virtual char* peer_block(int worker) = 0;                 // own blocks only
   virtual void set_peer_base(int worker, char* base) = 0;   // as addressable from this rank's device
   virtual void set_nccl(void* slice_comm, void* flat_comm) = 0;
+  // NVLS multicast average fan-out (nvls.cu, LSGD_B200_NVLS): wanted by this layout/config; gfull bytes per
+  // worker; bind this rank's gfull to the group's multicast object (after every member added its device)
+  virtual bool nvls_wanted() const = 0;
+  virtual size_t nvls_bytes() const = 0;
+  virtual void nvls_attach(uint64_t mc, size_t size, bool own_mc) = 0;
+  // processes: add this device to the group's object, wait until all k members have (flags in the leader's peer
+  // block, mapped at leader_block), then attach
+  virtual void nvls_join(uint64_t mc, size_t size, char* leader_block, int j, int k, double timeout_s) = 0;
   virtual void upload_dataset(const double* x, const int32_t* y, int64_t n) = 0;
   virtual void share_dataset_from(Rank* other) = 0;         // same-device or host-mapped dataset reuse
   virtual void set_params(const double* w) = 0;             // every local worker

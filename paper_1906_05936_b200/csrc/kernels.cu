@@ -537,6 +537,17 @@ __device__ __forceinline__ void gu_update_one(const GlobalUpdateArgs<T>& a, int6
   }
 }
 
+// One 16-byte store through an NVLS multicast address: the NVSwitch writes it into every bound member's memory.
+__device__ __forceinline__ void multimem_st(float* p, const Vec<float>& v) {
+  asm volatile("multimem.st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.v[0]), "f"(v.v[1]), "f"(v.v[2]),
+               "f"(v.v[3])
+               : "memory");
+}
+__device__ __forceinline__ void multimem_st(double* p, const Vec<double>& v) {
+  asm volatile("multimem.st.global.f64 [%0], %1;" ::"l"(p), "d"(v.v[0]) : "memory");  // (no .v2.f64 form)
+  asm volatile("multimem.st.global.f64 [%0], %1;" ::"l"(p + 1), "d"(v.v[1]) : "memory");
+}
+
 template <typename T, bool EXACT>
 __global__ void __launch_bounds__(256) global_update_kernel(const __grid_constant__ GlobalUpdateArgs<T> a,
                                                             bool vec_params) {
@@ -584,6 +595,7 @@ __global__ void __launch_bounds__(256) global_update_kernel(const __grid_constan
 #pragma unroll
       for (int q = 0; q < V; ++q) r.v[q] = Rn<T>::add(r.v[q], x.v[q]);
     }
+    if (a.mc) multimem_st(a.mc + e, r);  // NVLS: one store, replicated by the switch to every member
     for (int d = 0; d < a.n_push; ++d) st16(a.push.p[d] + e, r);  // broadcast to the other members
     if (a.out_local) st16(a.out_local + e, r);
     const int64_t i0 = a.first + e;
@@ -823,6 +835,7 @@ void launch_global_update(const GlobalUpdateArgs<T>& a, bool exact, cudaStream_t
     if (g != a.g) aligned = aligned && (reinterpret_cast<uintptr_t>(a.gsum.p[g]) & 15u) == 0;
   for (int d = 0; d < a.n_push; ++d) aligned = aligned && (reinterpret_cast<uintptr_t>(a.push.p[d]) & 15u) == 0;
   if (a.out_local) aligned = aligned && (reinterpret_cast<uintptr_t>(a.out_local) & 15u) == 0;
+  if (a.mc) aligned = aligned && (reinterpret_cast<uintptr_t>(a.mc) & 15u) == 0;
   check<Error>(aligned, "global_update: slices must be 16-byte aligned vectors");
   const bool vec_params = (reinterpret_cast<uintptr_t>(a.w + a.first) & 15u) == 0 &&
                           (a.v == nullptr || (reinterpret_cast<uintptr_t>(a.v + a.first) & 15u) == 0);

@@ -98,6 +98,7 @@ struct GlobalUpdateArgs {
   int G = 1, g = 0;
   bool gsum_raw = false; // k = 1: gstage holds the other owners' raw payload (DMA copy), apply (+0.0, /N) here
   bool direct = false;   // src holds all N = k*G sub-slices (group-major); every group's sum is formed here
+  T* mc = nullptr;       // NVLS: multicast view of the members' gfull at the slot; one multimem.st per vector
   bool add_zero = false;
   T divisor = T(0);
   int64_t len = 0;      // slot length S

@@ -1,0 +1,150 @@
+// NVLink SHARP (NVLS) multicast for the average fan-out of the push exchange (LSGD_B200_NVLS=1).
+//
+// The owner of slot j of group g pushes the slot's average to the k members' gfull. Unicast that is k-1 NVLink
+// stores per element (egress (k-1)*S per owner); through an NVSwitch multicast object bound to the k members'
+// gfull buffers it is ONE multimem.st per element: the switch replicates it to every member (egress S). A pure
+// copy, so the bits are those of the unicast push (no in-switch arithmetic — the reference's summation order is
+// kept by the owner's ordered sums).
+//
+// Object lifecycle (driver API, cuMulticast* / cuMem*): the group leader creates the multicast object; every member
+// adds its device, and only when all k have (a barrier) allocates its gfull as physical memory (cuMemCreate), binds
+// it to the object and maps both its local view and the multicast view. Processes share the object as a POSIX file
+// descriptor the members duplicate from the leader (pidfd_getfd); threads of one process share the handle.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <cstdint>
+
+#include "common.hpp"
+#include "nvls.hpp"
+
+namespace lsgd_b200 {
+
+#define LSGD_CU(expr)                                                                                          \
+  do {                                                                                                         \
+    CUresult r_ = (expr);                                                                                      \
+    if (r_ != CUDA_SUCCESS) {                                                                                  \
+      const char* s_ = nullptr;                                                                                \
+      cuGetErrorString(r_, &s_);                                                                               \
+      throw ::lsgd_b200::Error(::lsgd_b200::cat("CUDA driver error ", s_ ? s_ : "?", " (", static_cast<int>(r_), \
+                                                ") at ", __FILE__, ":", __LINE__, " (", #expr, ")"));          \
+    }                                                                                                          \
+  } while (0)
+
+namespace {
+CUmulticastObjectProp mc_prop(size_t size, int n_devices) {
+  CUmulticastObjectProp p{};
+  p.numDevices = static_cast<unsigned int>(n_devices);
+  p.size = size;
+  p.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  p.flags = 0;
+  return p;
+}
+size_t round_up_sz(size_t a, size_t b) { return (a + b - 1) / b * b; }
+}  // namespace
+
+size_t nvls_size(size_t bytes, int n_devices) {
+  LSGD_CU(cuInit(0));
+  CUmulticastObjectProp p = mc_prop(bytes, n_devices);
+  size_t g = 0;
+  LSGD_CU(cuMulticastGetGranularity(&g, &p, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+  return round_up_sz(bytes, g ? g : (2u << 20));
+}
+
+uint64_t nvls_create(size_t size, int n_devices, int* fd_out) {
+  LSGD_CU(cuInit(0));
+  CUmulticastObjectProp p = mc_prop(size, n_devices);
+  CUmemGenericAllocationHandle mc = 0;
+  LSGD_CU(cuMulticastCreate(&mc, &p));
+  if (fd_out) {
+    int fd = -1;
+    LSGD_CU(cuMemExportToShareableHandle(&fd, mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+    *fd_out = fd;
+  }
+  return static_cast<uint64_t>(mc);
+}
+
+uint64_t nvls_import(int pid, int fd) {
+  LSGD_CU(cuInit(0));
+  const int pidfd = static_cast<int>(syscall(SYS_pidfd_open, pid, 0));
+  check<Error>(pidfd >= 0, "NVLS: pidfd_open(", pid, ") failed");
+  const int local = static_cast<int>(syscall(SYS_pidfd_getfd, pidfd, fd, 0));
+  close(pidfd);
+  check<Error>(local >= 0, "NVLS: pidfd_getfd of the leader's multicast handle failed");
+  CUmemGenericAllocationHandle mc = 0;
+  CUresult r = cuMemImportFromShareableHandle(&mc, reinterpret_cast<void*>(static_cast<uintptr_t>(local)),
+                                              CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+  close(local);
+  LSGD_CU(r);
+  return static_cast<uint64_t>(mc);
+}
+
+void nvls_add_device(uint64_t mc, int dev) {
+  CUdevice d;
+  LSGD_CU(cuDeviceGet(&d, dev));
+  LSGD_CU(cuMulticastAddDevice(static_cast<CUmemGenericAllocationHandle>(mc), d));
+}
+
+void nvls_bind_map(NvlsBuffer& b, uint64_t mc, size_t size, int dev) {
+  LSGD_CUDA(cudaSetDevice(dev));
+  LSGD_CUDA(cudaFree(nullptr));  // the primary context is current
+  b.size = size;
+  b.dev = dev;
+  b.mc = mc;
+  CUmemAllocationProp ap{};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = dev;
+  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_NONE;
+  size_t gran = 0;
+  LSGD_CU(cuMemGetAllocationGranularity(&gran, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+  check<Error>(gran > 0 && size % gran == 0, "NVLS: buffer size ", size, " not a multiple of ", gran);
+  CUmemGenericAllocationHandle mem = 0;
+  LSGD_CU(cuMemCreate(&mem, size, &ap, 0));
+  b.mem = static_cast<uint64_t>(mem);
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = dev;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  CUdeviceptr va = 0;
+  LSGD_CU(cuMemAddressReserve(&va, size, gran, 0, 0));
+  LSGD_CU(cuMemMap(va, size, 0, mem, 0));
+  LSGD_CU(cuMemSetAccess(va, size, &acc, 1));
+  b.va = static_cast<uint64_t>(va);
+  LSGD_CU(cuMulticastBindMem(static_cast<CUmemGenericAllocationHandle>(mc), 0, mem, 0, size, 0));
+  CUdeviceptr mva = 0;
+  LSGD_CU(cuMemAddressReserve(&mva, size, gran, 0, 0));
+  LSGD_CU(cuMemMap(mva, size, 0, static_cast<CUmemGenericAllocationHandle>(mc), 0));
+  LSGD_CU(cuMemSetAccess(mva, size, &acc, 1));
+  b.mc_va = static_cast<uint64_t>(mva);
+  LSGD_CUDA(cudaMemset(reinterpret_cast<void*>(b.va), 0, size));
+  LSGD_CUDA(cudaDeviceSynchronize());
+}
+
+void nvls_free(NvlsBuffer& b) {
+  if (!b.size) return;
+  cudaSetDevice(b.dev);
+  cudaDeviceSynchronize();
+  CUdevice d;
+  if (cuDeviceGet(&d, b.dev) == CUDA_SUCCESS && b.mc)
+    cuMulticastUnbind(static_cast<CUmemGenericAllocationHandle>(b.mc), d, 0, b.size);
+  if (b.mc_va) {
+    cuMemUnmap(static_cast<CUdeviceptr>(b.mc_va), b.size);
+    cuMemAddressFree(static_cast<CUdeviceptr>(b.mc_va), b.size);
+  }
+  if (b.va) {
+    cuMemUnmap(static_cast<CUdeviceptr>(b.va), b.size);
+    cuMemAddressFree(static_cast<CUdeviceptr>(b.va), b.size);
+  }
+  if (b.mem) cuMemRelease(static_cast<CUmemGenericAllocationHandle>(b.mem));
+  if (b.mc && b.own_mc) cuMemRelease(static_cast<CUmemGenericAllocationHandle>(b.mc));
+  b = NvlsBuffer{};
+}
+
+void nvls_release(uint64_t mc) {
+  if (mc) cuMemRelease(static_cast<CUmemGenericAllocationHandle>(mc));
+}
+
+}  // namespace lsgd_b200

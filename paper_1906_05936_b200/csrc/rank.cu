@@ -27,6 +27,7 @@
 #include "engine.hpp"
 #include "gemm_tc.cuh"
 #include "kernels.cuh"
+#include "nvls.hpp"
 
 namespace lsgd_b200 {
 
@@ -261,6 +262,7 @@ class RankImpl final : public Rank {
     stop_nccl_watchdog();
     cudaSetDevice(dev_);
     cudaDeviceSynchronize();
+    nvls_free(nvls_);
     for (auto& kv : timers_)
       for (auto& pr : kv.second) {
         cudaEventDestroy(pr.first);
@@ -336,6 +338,40 @@ class RankImpl final : public Rank {
     flat_comm_ = static_cast<ncclComm_t>(flat_comm);
     if ((slice_comm_ || flat_comm_) && !nccl_watch_.joinable())
       nccl_watch_ = std::thread([this] { nccl_watch_loop(); });
+  }
+
+  // ---- NVLS multicast fan-out (nvls.cu): whole-slot push exchange, groups of k >= 2, LSGD_B200_NVLS=1
+  bool nvls_wanted() const override {
+    static const char* e = std::getenv("LSGD_B200_NVLS");
+    return e && std::atoi(e) != 0 && own_slot_fused() && k_ >= 2 && !sliced_global() && !direct_ && !pull_avg() &&
+           (G_ == 1 || spec_.c.global_algo == LSGD_B200_GLOBAL_ORDERED);
+  }
+  size_t nvls_bytes() const override { return static_cast<size_t>(geo_.Ppad) * sizeof(T); }
+  void nvls_join(uint64_t mc, size_t size, char* leader_block, int j, int k, double timeout_s) override {
+    LSGD_CUDA(cudaSetDevice(dev_));
+    nvls_add_device(mc, dev_);
+    auto* flags = reinterpret_cast<unsigned long long*>(leader_block + geo_.peer.flags) + kNvlsAdded;
+    const unsigned long long one = 1;
+    LSGD_CUDA(cudaMemcpy(flags + j, &one, sizeof(one), cudaMemcpyHostToDevice));
+    std::vector<unsigned long long> seen(static_cast<size_t>(k));
+    const double t0 = steady_s();
+    for (;;) {  // every member's device is in the team before anyone binds memory
+      LSGD_CUDA(cudaMemcpy(seen.data(), flags, sizeof(unsigned long long) * k, cudaMemcpyDeviceToHost));
+      bool all = true;
+      for (auto v : seen) all = all && v != 0;
+      if (all) break;
+      if (steady_s() - t0 > timeout_s)
+        throw TransportError(cat("NVLS: not every group member joined the multicast team within ", timeout_s, " s"));
+      std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
+    nvls_attach(mc, size, true);
+  }
+  void nvls_attach(uint64_t mc, size_t size, bool own_mc) override {
+    check<Error>(ws_.size() == 1, "NVLS needs one worker per GPU");
+    nvls_bind_map(nvls_, mc, size, dev_);
+    nvls_.own_mc = own_mc;
+    ws_[0].gfull = reinterpret_cast<T*>(nvls_.va);
+    mc_gfull_ = reinterpret_cast<T*>(nvls_.mc_va);
   }
 
   // ---- NCCL watchdog: the reference times out every receive (inprocess.cpp:44-49, TransportError). A collective
@@ -1709,6 +1745,11 @@ class RankImpl final : public Rank {
         ga.n_push = 0;
         ga.out_local = w.gbar + bk.goff + p0;
       }
+      int n_signal = ga.n_push;  // members whose arrival flag this owner releases
+      if (mc_gfull_ && !sl) {    // NVLS: one multicast store per vector instead of k-1 unicast pushes
+        ga.mc = mc_gfull_ + bk.poff + static_cast<int64_t>(me) * bk.S + p0;
+        ga.n_push = 0;
+      }
       DstList<T> remote = ga.push;
       const int n_remote = ga.n_push;
       const bool fan_dma = dma(8) && n_remote > 0;
@@ -1729,8 +1770,8 @@ class RankImpl final : public Rank {
         for (int d = 0; d < N_; ++d)
           if (d != w.id && d / k_ == w.g) mem.f[nm++] = peer_arrived(d, b, arr);
         if (nm) launch_signal_many(mem, nm, round, st, lc_);
-      } else if (n_remote) {
-        launch_signal_many(others, n_remote, round, st, lc_);
+      } else if (n_signal) {
+        launch_signal_many(others, n_signal, round, st, lc_);
       }
       LSGD_CUDA(cudaEventRecord(ev_gupd_[b], st));
       return;
@@ -2087,6 +2128,8 @@ class RankImpl final : public Rank {
   std::vector<int32_t*> own_y_;  // per layer: dX_k issued (W_k free for its update)
   cudaStream_t upd_ = nullptr;
   bool direct_ = false;  // direct two-hop exchange (LSGD_B200_DIRECT)
+  NvlsBuffer nvls_;       // NVLS: this worker's gfull bound to the group's multicast object
+  T* mc_gfull_ = nullptr; // its multicast view (null: unicast pushes)
   cudaStream_t iod_ = nullptr;  // emulated ranks: the injected io latency, overlapping the previous exchange
   cudaEvent_t ev_pre_exch_ = nullptr, ev_io_done_ = nullptr;
   std::vector<char*> peer_base_;

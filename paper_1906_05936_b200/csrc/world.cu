@@ -11,6 +11,7 @@
 #include <thread>
 
 #include "engine.hpp"
+#include "nvls.hpp"
 
 namespace lsgd_b200 {
 
@@ -124,6 +125,19 @@ void run_world(const RunSpec& spec, bool want_history, bool want_workers, TrainO
     for (int i = 0; i < N; ++i) ranks[static_cast<size_t>(i)]->set_nccl(nullptr, cs[static_cast<size_t>(i)]);
   }
 
+  // NVLS multicast fan-out (LSGD_B200_NVLS): one object per group, every member's device added before any binds;
+  // the handles stay with this function until the ranks are gone
+  std::vector<uint64_t> mcs;
+  if (one_each && ranks[0]->nvls_wanted()) {
+    for (int g = 0; g < G; ++g) {
+      const size_t size = nvls_size(ranks[static_cast<size_t>(g * k)]->nvls_bytes(), k);
+      const uint64_t mc = nvls_create(size, k, nullptr);
+      mcs.push_back(mc);
+      for (int m = 0; m < k; ++m) nvls_add_device(mc, ranks[static_cast<size_t>(g * k + m)]->device());
+      for (int m = 0; m < k; ++m) ranks[static_cast<size_t>(g * k + m)]->nvls_attach(mc, size, false);
+    }
+  }
+
   // inputs: host-generated with the reference-identical streams, data = seed, init = seed + 1
   if (spec.c.model == LSGD_B200_MODEL_MLP) {
     const int64_t n = spec.c.n_samples;
@@ -203,6 +217,7 @@ void run_world(const RunSpec& spec, bool want_history, bool want_workers, TrainO
   out.launches = 0;
   for (auto& r : ranks) out.launches += r->launches();
   ranks.clear();  // destroys comms too (each rank owns its handles)
+  for (uint64_t mc : mcs) nvls_release(mc);
 }
 
 }  // namespace lsgd_b200

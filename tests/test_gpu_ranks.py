@@ -296,3 +296,45 @@ def test_direct_exchange_is_bitwise_the_three_hop_form(groups, per_group, dtype,
         spec = TrainSpec(**{k: getattr(cfg, k) for k in TrainSpec.__dataclass_fields__ if hasattr(cfg, k)})
         ref = Oracle("port").run_train(spec)["final_params"]
         assert (np.abs(d[0] - ref) / np.maximum(np.abs(ref), 1e-8)).max() <= 1e-8
+
+
+@pytest.mark.parametrize("groups,per_group,dtype", [(1, 4, "fp32"), (1, 4, "fp64"), (2, 2, "fp32"), (1, 2, "fp64")])
+def test_nvls_multicast_fanout_is_bitwise_the_unicast_push(groups, per_group, dtype, n_gpus):
+    """LSGD_B200_NVLS: the slot owner stores each averaged vector once into an NVSwitch multicast object bound to
+    its group's gfull buffers (multimem.st) instead of k-1 unicast NVLink stores — a copy, so the same bits; fp64
+    also per-coordinate on the oracle. One process per GPU (the object is shared as a file descriptor)."""
+    n = groups * per_group
+    if n_gpus < n:
+        pytest.skip(f"needs {n} GPUs")
+    mc = _spawn(n, dtype, groups, "train", env={"LSGD_B200_NVLS": "1"})
+    uc = _spawn(n, dtype, groups, "train", env={"LSGD_B200_NVLS": "0"})
+    for q in range(n):
+        assert np.array_equal(mc[q].view(np.uint64), uc[q].view(np.uint64)), q
+    if dtype == "fp64":
+        from oracle import Oracle, TrainSpec
+        cfg = _cfg(dtype, n, groups)
+        spec = TrainSpec(**{k: getattr(cfg, k) for k in TrainSpec.__dataclass_fields__ if hasattr(cfg, k)})
+        ref = Oracle("port").run_train(spec)["final_params"]
+        assert (np.abs(mc[0] - ref) / np.maximum(np.abs(ref), 1e-8)).max() <= 1e-8
+
+
+def test_nvls_in_the_threaded_world(n_gpus):
+    """The same multicast fan-out in the one-process world (run_train, one host thread per GPU): 1x4 fp64 on the
+    oracle per coordinate."""
+    if n_gpus < 4:
+        pytest.skip("needs 4 GPUs")
+    import subprocess
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r)\\n"
+        "from test_gpu_ranks import _cfg\\n"
+        "import paper_1906_05936_b200 as lsgd\\n"
+        "from oracle import Oracle, TrainSpec\\n"
+        "cfg = _cfg('fp64', 4, 1); cfg.b200.n_devices = 4\\n"
+        "w = lsgd.run_train(cfg).final_params\\n"
+        "spec = TrainSpec(**{k: getattr(cfg, k) for k in TrainSpec.__dataclass_fields__ if hasattr(cfg, k)})\\n"
+        "ref = Oracle('port').run_train(spec)['final_params']\\n"
+        "print((np.abs(w - ref) / np.maximum(np.abs(ref), 1e-8)).max())\\n" % (ROOT, os.path.join(ROOT, "tests")))
+    out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, LSGD_B200_NVLS="1"), cwd=ROOT,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    assert float(out.stdout.strip().splitlines()[-1]) <= 1e-8
