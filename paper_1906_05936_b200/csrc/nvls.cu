@@ -97,10 +97,16 @@ void nvls_bind_map(NvlsBuffer& b, uint64_t mc, size_t size, int dev) {
   ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   ap.location.id = dev;
-  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_NONE;
+  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;  // as NCCL's NVLS buffers
   size_t gran = 0;
-  LSGD_CU(cuMemGetAllocationGranularity(&gran, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+  LSGD_CU(cuMemGetAllocationGranularity(&gran, &ap, CU_MEM_ALLOC_GRANULARITY_MINIMUM));
   check<Error>(gran > 0 && size % gran == 0, "NVLS: buffer size ", size, " not a multiple of ", gran);
+  size_t mgran = 0;  // the multicast object's granularity aligns the mappings
+  {
+    CUmulticastObjectProp p = mc_prop(size, 1);
+    LSGD_CU(cuMulticastGetGranularity(&mgran, &p, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+    if (mgran < gran) mgran = gran;
+  }
   CUmemGenericAllocationHandle mem = 0;
   LSGD_CU(cuMemCreate(&mem, size, &ap, 0));
   b.mem = static_cast<uint64_t>(mem);
@@ -109,13 +115,13 @@ void nvls_bind_map(NvlsBuffer& b, uint64_t mc, size_t size, int dev) {
   acc.location.id = dev;
   acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
   CUdeviceptr va = 0;
-  LSGD_CU(cuMemAddressReserve(&va, size, gran, 0, 0));
+  LSGD_CU(cuMemAddressReserve(&va, size, mgran, 0, 0));
   LSGD_CU(cuMemMap(va, size, 0, mem, 0));
   LSGD_CU(cuMemSetAccess(va, size, &acc, 1));
   b.va = static_cast<uint64_t>(va);
   LSGD_CU(cuMulticastBindMem(static_cast<CUmemGenericAllocationHandle>(mc), 0, mem, 0, size, 0));
   CUdeviceptr mva = 0;
-  LSGD_CU(cuMemAddressReserve(&mva, size, gran, 0, 0));
+  LSGD_CU(cuMemAddressReserve(&mva, size, mgran, 0, 0));
   LSGD_CU(cuMemMap(mva, size, 0, static_cast<CUmemGenericAllocationHandle>(mc), 0));
   LSGD_CU(cuMemSetAccess(mva, size, &acc, 1));
   b.mc_va = static_cast<uint64_t>(mva);
