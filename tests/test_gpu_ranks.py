@@ -325,15 +325,15 @@ def test_nvls_in_the_threaded_world(n_gpus):
         pytest.skip("needs 4 GPUs")
     import subprocess
     code = (
-        "import sys, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r)\\n"
-        "from test_gpu_ranks import _cfg\\n"
-        "import paper_1906_05936_b200 as lsgd\\n"
-        "from oracle import Oracle, TrainSpec\\n"
-        "cfg = _cfg('fp64', 4, 1); cfg.b200.n_devices = 4\\n"
-        "w = lsgd.run_train(cfg).final_params\\n"
-        "spec = TrainSpec(**{k: getattr(cfg, k) for k in TrainSpec.__dataclass_fields__ if hasattr(cfg, k)})\\n"
-        "ref = Oracle('port').run_train(spec)['final_params']\\n"
-        "print((np.abs(w - ref) / np.maximum(np.abs(ref), 1e-8)).max())\\n" % (ROOT, os.path.join(ROOT, "tests")))
+        "import sys, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "from test_gpu_ranks import _cfg\n"
+        "import paper_1906_05936_b200 as lsgd\n"
+        "from oracle import Oracle, TrainSpec\n"
+        "cfg = _cfg('fp64', 4, 1); cfg.b200.n_devices = 4\n"
+        "w = lsgd.run_train(cfg).final_params\n"
+        "spec = TrainSpec(**{k: getattr(cfg, k) for k in TrainSpec.__dataclass_fields__ if hasattr(cfg, k)})\n"
+        "ref = Oracle('port').run_train(spec)['final_params']\n"
+        "print((np.abs(w - ref) / np.maximum(np.abs(ref), 1e-8)).max())\n" % (ROOT, os.path.join(ROOT, "tests")))
     out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, LSGD_B200_NVLS="1"), cwd=ROOT,
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
