@@ -36,7 +36,8 @@ int lsgd_b200_test_rank_timeline(lsgd_b200_rank* r, char* buf, int64_t cap);
  * 1..n_dev-1 over NVLink, so a profiler can replay it: kind 0 = K6 reduce_push (k local sub-slices summed, +0.0, /N,
  * pushed to 1 local + n_dev-1 remote owners), 1 = member->owner scatter with SM stores (n_dev-1 pairs), 2 = K7+K8
  * global_update of the owner's slot (k sub-slices + 1 group sum, momentum update, average pushed to n_dev-1
- * members), 3 = K8 update (local), 4 = copy-engine peer copies (n_dev-1). len = slot elements (fp32). Returns the
+ * members), 3 = K8 update (local), 4 = copy-engine peer copies (n_dev-1), 5 = kind 2 with the NVLS multicast
+ * fan-out (one multimem.st per vector into the n_dev devices' buffers). len = slot elements (fp32). Returns the
  * average device time over reps launches and the algorithmic NVLink / local HBM bytes of one launch. */
 int lsgd_b200_test_exchange_kernel(int32_t kind, int32_t n_dev, int32_t k, int64_t len, int32_t reps, double* avg_ms,
                                    double* bytes_nvlink, double* bytes_local);

@@ -11,6 +11,7 @@
 #include "../../include/lsgd_b200_testing.h"
 #include "common.hpp"
 #include "kernels.cuh"
+#include "nvls.hpp"
 
 using namespace lsgd_b200;
 
@@ -69,6 +70,21 @@ extern "C" int lsgd_b200_test_exchange_kernel(int32_t kind, int32_t n_dev, int32
     LSGD_CUDA(cudaMalloc(&bad, sizeof(unsigned)));
     for (size_t m = 0; m < src.size(); ++m) fill_kernel<<<592, 256>>>(src[m], len, 0.1f * static_cast<float>(m + 1));
     fill_kernel<<<592, 256>>>(w, len, 0.5f);
+    std::vector<NvlsBuffer> mcb;
+    uint64_t mc = 0;
+    float* mc_ptr = nullptr;
+    if (kind == 5) {  // one multicast object over n_dev devices, each binding len floats
+      const size_t size = nvls_size(sizeof(float) * static_cast<size_t>(len), n_dev);
+      mc = nvls_create(size, n_dev, nullptr);
+      for (int d = 0; d < n_dev; ++d) nvls_add_device(mc, d);
+      mcb.resize(static_cast<size_t>(n_dev));
+      for (int d = 0; d < n_dev; ++d) {
+        nvls_bind_map(mcb[static_cast<size_t>(d)], mc, size, d);
+        mcb[static_cast<size_t>(d)].own_mc = false;
+      }
+      mc_ptr = reinterpret_cast<float*>(mcb[0].mc_va);
+      LSGD_CUDA(cudaSetDevice(0));
+    }
     cudaStream_t st;
     LSGD_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     LaunchCounter lc;
@@ -143,6 +159,30 @@ extern "C" int lsgd_b200_test_exchange_kernel(int32_t kind, int32_t n_dev, int32
           loc = 20.0 * len;
           break;
         }
+        case 5: {  // kind 2 with the NVLS fan-out: one multimem.st per vector into the n_dev members' buffers
+          GlobalUpdateArgs<float> a;
+          for (int m = 0; m < k; ++m) a.src.p[m] = src[static_cast<size_t>(m)];
+          a.k = k;
+          a.gsum.p[1] = src[1];
+          a.G = 2;
+          a.g = 0;
+          a.add_zero = true;
+          a.divisor = 4.0f;
+          a.len = len;
+          a.mc = mc_ptr;
+          a.n_params = len;
+          a.w = w;
+          a.v = v;
+          a.mode = 1;
+          a.lr = 1e-3f;
+          a.momentum = 0.9f;
+          a.weight_decay = 1e-4f;
+          a.bad = bad;
+          launch_global_update<float>(a, false, st, lc);
+          nv = 4.0 * len;  // one copy leaves this GPU; the switch replicates it to the n_dev members
+          loc = 4.0 * len * (k + 1 + 4);
+          break;
+        }
         case 4: {  // copy-engine peer copies (the LSGD_B200_DMA path): R concurrent copies local -> remote
           for (int r = 0; r < R; ++r)
             LSGD_CUDA(cudaMemcpyAsync(remote[static_cast<size_t>(r)], src[static_cast<size_t>(r % src.size())],
@@ -173,6 +213,9 @@ extern "C" int lsgd_b200_test_exchange_kernel(int32_t kind, int32_t n_dev, int32
     cudaEventDestroy(e1);
     cudaStreamDestroy(st);
     cudaFree(bad);
+    for (auto& b : mcb) nvls_free(b);
+    if (mc) nvls_release(mc);
+    LSGD_CUDA(cudaSetDevice(0));
     return LSGD_B200_OK;
   } catch (const ConfigError& e) {
     last_error_slot() = e.what();

@@ -16,7 +16,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 KINDS = {0: "reduce_push (K6 owner sum + push)", 1: "copy_pairs (scatter, SM stores)",
-         2: "global_update (K7+K8 own slot + push)", 3: "update (K8, local)", 4: "cudaMemcpyAsync peer (copy engine)"}
+         2: "global_update (K7+K8 own slot + push)", 3: "update (K8, local)", 4: "cudaMemcpyAsync peer (copy engine)",
+         5: "global_update + NVLS multimem.st fan-out"}
 
 
 def main():
