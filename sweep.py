@@ -92,9 +92,15 @@ def main():
             line["scatter_nvlink_gbs"] = gbs((k - 1) * S, worst["scatter"]) if k > 1 else None
             line["reduce_push_gbs"] = gbs((G - 1) * S, worst["reduce"]) if G > 1 else None
             line["push_nvlink_gbs"] = gbs((k - 1) * S, worst["broadcast"]) if k > 1 else None
-            line["global_busbw_gbs"] = gbs(2 * (G - 1) / G * S, worst["global"]) if G > 1 else None
+            sliced = G > 2 or (G > 1 and k == 1)  # the engine's default (rank.cu sliced_global)
+            if args.global_allreduce == "nccl":
+                line["global_busbw_gbs"] = gbs(2 * (G - 1) / G * S, worst["global"]) if G > 1 else None
+            else:  # fused global kernel: ordered group sum + update of the own slot (piece) + fan-out of its average
+                line["global_push_gbs"] = gbs((world - 1) * S / G if sliced else (k - 1) * S, worst["global"])
             line["global_allreduce"] = args.global_allreduce
-            line["update_hbm_gbs"] = gbs(20.0 * P, worst["update"])
+            # the update kernel covers the slots (pieces) this GPU does not own: 20 B per parameter (momentum)
+            own = (1.0 / world if sliced else 1.0 / k) if world > 1 else 0.0
+            line["update_hbm_gbs"] = gbs(20.0 * P * (1.0 - own), worst["update"])
             line["nvlink_peak_gbs"] = NVLINK_GBS
             line["hbm_peak_gbs"] = hbm
             print(json.dumps(line), flush=True)
