@@ -136,15 +136,16 @@ def cpu_reference(cfg_name: str, n: int, steps: int, warmup: int, bloc: int | No
     from oracle import Oracle, TrainSpec
 
     cores = os.cpu_count() or 1
-    # libgomp reads OMP_NUM_THREADS when the reference library loads; the survey found OpenMP per-sample passes
-    # slower than serial, so the rank threads supply the parallelism and OpenMP gets the remaining cores.
-    os.environ.setdefault("OMP_NUM_THREADS", str(max(1, min(cores, 8) // max(1, n))))
+    # every host thread the box has: each of the n worker ranks gets cores / n OpenMP threads for its per-sample
+    # passes (batch_gradient parallelises over the samples of a 32-sample block, mlp.cpp:249-257), and B_loc matches
+    # that thread count so none idles. libgomp reads OMP_NUM_THREADS when the reference library loads.
+    os.environ.setdefault("OMP_NUM_THREADS", str(max(1, cores // max(1, n))))
     ref = Oracle("reference")
     if cfg_name == "cfg3":
         # OpenMP gradient scratch is min(32, B) x P doubles (mlp.cpp:243-245): keep B_loc small, dataset small
         # bounded sample (~10-60 s of CPU work whatever --steps is): a few iterations at a small per-worker batch;
         # the reference's per-sample cost does not depend on the batch or dataset size
-        b = max(1, min(8, cores // max(1, n)))
+        b = max(1, min(32, cores // max(1, n)))
         iters = max(1, min(steps, 3))
         spec = TrainSpec(algorithm=algo, n_workers=n, n_groups=(groups or min(2, n)) if algo == "lsgd" else 1,
                          layer_sizes=[4096, 8192, 8192, 512], n_samples=max(1024, 4 * b * n), n_features=4096,
