@@ -1,5 +1,8 @@
-# N=4 (2x2) bench by update-kernel grid cap / unroll, one box
-for cfg in "1184 1" "296 1" "592 1" "1184 2" "1184 1"; do
-  set -- $cfg
-  echo "N4 upd_ctas=$1 unroll=$2 $(LSGD_B200_UPD_CTAS=$1 LSGD_B200_UPD_UNROLL=$2 timeout -s KILL 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port $((29400 + $1 % 97 + $2)) bench.py --gpus 4 --skip-e2e 2>/dev/null | tail -1 | python -c 'import json,sys; l=json.loads(sys.stdin.read()); print(round(l["value"]), l["ms_per_step"])')"
+run() {
+  echo "$1 => $(env $1 timeout -s KILL 300 python bench.py --skip-e2e --skip-cpu 2>/dev/null | tail -1 | python -c 'import json,sys; l=json.loads(sys.stdin.read()); k=l["kernels"]; print(round(l["value"]), round(l["ms_per_step"],4), "gemm", round(k["gemm"]["ms_per_step"],4), "upd", round(k["update"]["avg_ms"],4))')"
+}
+for rep in 1 2; do
+for v in "X=0" "LSGD_B200_UPD_CTAS=296 LSGD_B200_UPD_UNROLL=2" "LSGD_B200_UPD_CTAS=296 LSGD_B200_UPD_UNROLL=4" "LSGD_B200_UPD_CTAS=148 LSGD_B200_UPD_UNROLL=4" "LSGD_B200_UPD_CTAS=592 LSGD_B200_UPD_UNROLL=2" "LSGD_B200_UPD_CTAS=296"; do
+  run "$v"
+done
 done
