@@ -398,7 +398,17 @@ def run_b200_arm(args):
             step_roof = {"t_roof_ms": t_roof * 1e3, "t_step_ms": ms_max / args.steps,
                          "frac": t_roof * 1e3 / (ms_max / args.steps), "t_gemm_ms": t_gemm * 1e3,
                          "t_nvlink_ms": t_link * 1e3,
-                         "basis": "3xTF32 = bf16_tflops_sustained/6; NVLink 900 GB/s per direction"}
+                         "basis": "SURVEY.md §8(d): 3xTF32 = bf16_tflops_sustained/6; 4(P+1) B over NVLink 900 GB/s"}
+            # the same bound with the measured ceilings: split-TF32 = measured TF32 / 3, and the exchange's
+            # algorithmic egress 2(N-1)/N * 4(P+1) B at the measured 770 GB/s peer bandwidth
+            try:
+                tf32 = json.load(open(os.path.join(ROOT, "profiles", "r2_tf32_peak.json")))["tf32_tflops_sustained"]
+                t_g = B * flops_per_sample(cfg.layer_sizes) / (tf32 / 3.0 * 1e12)
+                t_l = 2.0 * (n - 1) / n * 4.0 * (cfg.n_params + 1) / 770e9 if n > 1 else 0.0
+                step_roof["measured"] = {"t_gemm_ms": t_g * 1e3, "t_nvlink_ms": t_l * 1e3,
+                                         "frac": max(t_g, t_l) / (ms_max / args.steps / 1e3)}
+            except (OSError, ValueError, KeyError):
+                pass
         kern = {f: {"avg_ms": v[0], "count": v[1], "ms_per_step": v[0] * v[1] / args.steps}
                 for f, v in fams.items() if v[1]}
         # exposed communication (BASELINE metric): step time not covered by the main stream's compute kernels
