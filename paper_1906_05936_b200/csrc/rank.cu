@@ -314,6 +314,9 @@ class RankImpl final : public Rank {
     for (int b = 0; b < kMaxBuckets; ++b) cudaEventDestroy(ev_gupd_[b]);
     cudaEventDestroy(join_ev_);
     if (iod_) cudaStreamDestroy(iod_);
+    if (pio_) cudaStreamDestroy(pio_);
+    if (ev_x_free_) cudaEventDestroy(ev_x_free_);
+    if (ev_x_ready_) cudaEventDestroy(ev_x_ready_);
     if (ev_pre_exch_) cudaEventDestroy(ev_pre_exch_);
     if (ev_io_done_) cudaEventDestroy(ev_io_done_);
     if (base_ev_) cudaEventDestroy(base_ev_);
@@ -1069,25 +1072,51 @@ class RankImpl final : public Rank {
       for (size_t i = 0; i < ws_.size(); ++i) phase_mark(i, t, 0, 0, main_);
       launch_sleep(spec_.c.io_delay_s, main_, lc_);
     }
+    // Prefetched io (one worker per GPU, no injected delay): the gather of step t runs on its own stream as soon as
+    // step t-1 no longer reads the batch buffers (after its last layer-0 weight-gradient GEMM, ev_x_free_), i.e.
+    // under the rest of t-1's backward, instead of on the main stream between the two steps. Same kernel, same
+    // rows. LSGD_B200_PREFETCH_IO=0 keeps it on the main stream.
+    const bool pre = prefetch_io();
+    cudaStream_t ist = main_;
+    if (pre) {
+      if (!pio_) {
+        int lo = 0, hi = 0;
+        LSGD_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        LSGD_CUDA(cudaStreamCreateWithPriority(&pio_, cudaStreamNonBlocking, hi));
+        LSGD_CUDA(cudaEventCreateWithFlags(&ev_x_free_, cudaEventDisableTiming));
+        LSGD_CUDA(cudaEventCreateWithFlags(&ev_x_ready_, cudaEventDisableTiming));
+      }
+      if (x_free_recorded_) LSGD_CUDA(cudaStreamWaitEvent(pio_, ev_x_free_, 0));
+      ist = pio_;
+    }
     for (size_t i = 0; i < ws_.size(); ++i) {
       Worker& w = ws_[i];
       if (!emu_delay) {
-        phase_mark(i, t, 0, 0, main_);
-        launch_sleep(spec_.c.io_delay_s, main_, lc_);
+        phase_mark(i, t, 0, 0, ist);
+        launch_sleep(spec_.c.io_delay_s, ist, lc_);
       }
-      LSGD_CUDA(cudaMemcpyAsync(w.idx, dst + i * B_, sizeof(int32_t) * B_, cudaMemcpyHostToDevice, main_));
+      LSGD_CUDA(cudaMemcpyAsync(w.idx, dst + i * B_, sizeof(int32_t) * B_, cudaMemcpyHostToDevice, ist));
       {
-        Timed tm(this, "gather", main_);
+        Timed tm(this, "gather", ist);
         if (use_tc_ && spec_.c.n_features % 4 == 0) {  // rows straight into the first GEMM's TF32 split
-          tc_gather_split(w.tc, L_, reinterpret_cast<const float*>(data_x_), data_y_, w.idx, w.y, main_, lc_);
+          tc_gather_split(w.tc, L_, reinterpret_cast<const float*>(data_x_), data_y_, w.idx, w.y, ist, lc_);
           w.x_split_ready = true;
         } else {
-          launch_gather<T>(data_x_, data_y_, w.idx, B_, spec_.c.n_features, w.x, w.y, main_, lc_);
+          launch_gather<T>(data_x_, data_y_, w.idx, B_, spec_.c.n_features, w.x, w.y, ist, lc_);
         }
       }
-      phase_mark(i, t, 0, 1, main_);
+      phase_mark(i, t, 0, 1, ist);
     }
-    LSGD_CUDA(cudaEventRecord(ring_ev_[slot], main_));
+    LSGD_CUDA(cudaEventRecord(ring_ev_[slot], ist));
+    if (pre) {
+      LSGD_CUDA(cudaEventRecord(ev_x_ready_, pio_));
+      LSGD_CUDA(cudaStreamWaitEvent(main_, ev_x_ready_, 0));
+    }
+  }
+  bool prefetch_io() const {
+    static const char* e = std::getenv("LSGD_B200_PREFETCH_IO");
+    const bool on = e ? std::atoi(e) != 0 : true;
+    return on && split_ && !synth_ && spec_.c.io_delay_s <= 0 && !fused_update();
   }
 
   // ------------------------------------------------------------------------------------------ compute
@@ -1951,6 +1980,10 @@ class RankImpl final : public Rank {
           if (exchange && !split_) signal(w, kFlagGrad, b, static_cast<unsigned long long>(t + 1), main_);
           if (split_) LSGD_CUDA(cudaEventRecord(ev_bucket_[b], main_));
         }
+        if (pio_ && op.layer == 0 && op.buckets.back() == LB[0].back()) {  // the batch buffers are free for t+1
+          LSGD_CUDA(cudaEventRecord(ev_x_free_, main_));
+          x_free_recorded_ = true;
+        }
       }
       phase_mark(widx(w), t, 1, 1, main_);
     }
@@ -2128,6 +2161,9 @@ class RankImpl final : public Rank {
   std::vector<int32_t*> own_y_;  // per layer: dX_k issued (W_k free for its update)
   cudaStream_t upd_ = nullptr;
   bool direct_ = false;  // direct two-hop exchange (LSGD_B200_DIRECT)
+  cudaStream_t pio_ = nullptr;  // prefetched io (gather of the next step under the current backward)
+  cudaEvent_t ev_x_free_ = nullptr, ev_x_ready_ = nullptr;
+  bool x_free_recorded_ = false;
   NvlsBuffer nvls_;       // NVLS: this worker's gfull bound to the group's multicast object
   T* mc_gfull_ = nullptr; // its multicast view (null: unicast pushes)
   cudaStream_t iod_ = nullptr;  // emulated ranks: the injected io latency, overlapping the previous exchange
