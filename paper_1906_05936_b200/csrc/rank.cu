@@ -1075,7 +1075,9 @@ class RankImpl final : public Rank {
     // Prefetched io (one worker per GPU, no injected delay): the gather of step t runs on its own stream as soon as
     // step t-1 no longer reads the batch buffers (after its last layer-0 weight-gradient GEMM, ev_x_free_), i.e.
     // under the rest of t-1's backward, instead of on the main stream between the two steps. Same kernel, same
-    // rows. LSGD_B200_PREFETCH_IO=0 keeps it on the main stream.
+    // rows. Off by default (LSGD_B200_PREFETCH_IO=1): the gather's 512 latency-bound CTAs under the dW_1 GEMM slow
+    // it more than the 12-90 us they take off the step boundary (N = 1: 339k vs 351k samples/s, N = 4: 982k vs
+    // 1.002M; profiles/r2_prefetch_io_ab.log).
     const bool pre = prefetch_io();
     cudaStream_t ist = main_;
     if (pre) {
@@ -1115,7 +1117,7 @@ class RankImpl final : public Rank {
   }
   bool prefetch_io() const {
     static const char* e = std::getenv("LSGD_B200_PREFETCH_IO");
-    const bool on = e ? std::atoi(e) != 0 : true;
+    const bool on = e ? std::atoi(e) != 0 : false;
     return on && split_ && !synth_ && spec_.c.io_delay_s <= 0 && !fused_update();
   }
 
