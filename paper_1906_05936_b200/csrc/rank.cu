@@ -1543,7 +1543,10 @@ class RankImpl final : public Rank {
     int n = 0;
     for (int q = 0; q < n_words; ++q)
       if (q != skip) fl.f[n++] = w.flags + first + q;
-    if (n) launch_wait_flags(fl, n, target, timeout_ns(), timed_out_dev_, st, lc_, max_lead);
+    if (n) {
+      Timed tm(this, "wait", st);  // timeline only: when this rank's peers' data for the stage arrived
+      launch_wait_flags(fl, n, target, timeout_ns(), timed_out_dev_, st, lc_, max_lead);
+    }
   }
   // Direct two-hop exchange (direct_exchange(), engine.hpp): this GPU's sub-slice j goes by copy engine to the
   // slot-j owner of every group (stage[par][my id]); the owner of slot `me` then sums all N sub-slices in the
