@@ -4,6 +4,7 @@
 // GPUs. Rounding: in EXACT mode every multiply and add rounds separately (no FMA contraction), reproducing the
 // reference's x86-64 build operation for operation (mlp.cpp:70-75, 110-123, 262-271; transport.cpp:27-48;
 // optimizer.cpp:30-38).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -851,7 +852,36 @@ void launch_global_update(const GlobalUpdateArgs<T>& a, bool exact, cudaStream_t
   LSGD_CUDA(cudaGetLastError());
 }
 
+// Release of cross-GPU round counters after the prior work of the stream. By default a stream memory operation
+// (cuStreamWriteValue64, executed by the GPU front end with a system-wide fence before the write): it needs no SM,
+// so a flag is released as soon as its copy or kernel ends even when long-running kernels hold every SM's thread
+// slots (a 1-CTA signal kernel then waits for them — up to ~200 us per hop, profiles/r2_timeline_n4_waits.txt).
+// LSGD_B200_SIGNAL_MEMOP=0: the signal kernel.
+using StreamWriteValue64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+StreamWriteValue64 stream_write_value64() {
+  static StreamWriteValue64 fn = [] {
+    const char* e = std::getenv("LSGD_B200_SIGNAL_MEMOP");
+    if (e && std::atoi(e) == 0) return static_cast<StreamWriteValue64>(nullptr);
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return static_cast<StreamWriteValue64>(nullptr);
+    }
+    return reinterpret_cast<StreamWriteValue64>(p);
+  }();
+  return fn;
+}
+
 void launch_signal_many(SignalList flags, int n, unsigned long long value, cudaStream_t st, LaunchCounter& lc) {
+  if (StreamWriteValue64 wv = stream_write_value64()) {
+    for (int i = 0; i < n; ++i) {
+      const CUresult r = wv(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(flags.f[i]), value, 0);
+      check<Error>(r == CUDA_SUCCESS, "cuStreamWriteValue64 failed (", static_cast<int>(r), ")");
+    }
+    return;
+  }
   signal_many_kernel<<<1, 32, 0, st>>>(flags, n, value);
   ++lc.n;
   LSGD_CUDA(cudaGetLastError());
