@@ -876,8 +876,9 @@ StreamWriteValue64 stream_write_value64() {
 
 void launch_signal_many(SignalList flags, int n, unsigned long long value, cudaStream_t st, LaunchCounter& lc) {
   if (StreamWriteValue64 wv = stream_write_value64()) {
-    for (int i = 0; i < n; ++i) {
-      const CUresult r = wv(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(flags.f[i]), value, 0);
+    for (int i = 0; i < n; ++i) {  // one system-wide fence (before the first write) covers the stream's prior work
+      const CUresult r = wv(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(flags.f[i]), value,
+                            i == 0 ? 0u : static_cast<unsigned>(CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER));
       check<Error>(r == CUDA_SUCCESS, "cuStreamWriteValue64 failed (", static_cast<int>(r), ")");
     }
     return;
