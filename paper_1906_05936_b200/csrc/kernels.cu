@@ -875,12 +875,13 @@ StreamWriteValue64 stream_write_value64() {
 }
 
 void launch_signal_many(SignalList flags, int n, unsigned long long value, cudaStream_t st, LaunchCounter& lc) {
-  if (StreamWriteValue64 wv = stream_write_value64()) {
-    for (int i = 0; i < n; ++i) {  // one system-wide fence (before the first write) covers the stream's prior work
-      const CUresult r = wv(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(flags.f[i]), value,
-                            i == 0 ? 0u : static_cast<unsigned>(CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER));
-      check<Error>(r == CUDA_SUCCESS, "cuStreamWriteValue64 failed (", static_cast<int>(r), ")");
-    }
+  // One destination: the memop. Several: one kernel (one fence, n stores) — each fenced memop costs more than the
+  // kernel saves there, and dropping the fence on the later writes is not safe (A/B: 1x4 / 4x1 -4..5% with a memop
+  // per flag, 2x2 +1.4% with memops; profiles/r2_signal_memop_ab.log).
+  StreamWriteValue64 wv = n == 1 ? stream_write_value64() : nullptr;
+  if (wv) {
+    const CUresult r = wv(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(flags.f[0]), value, 0);
+    check<Error>(r == CUDA_SUCCESS, "cuStreamWriteValue64 failed (", static_cast<int>(r), ")");
     return;
   }
   signal_many_kernel<<<1, 32, 0, st>>>(flags, n, value);
