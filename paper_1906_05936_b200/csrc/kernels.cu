@@ -769,8 +769,36 @@ void launch_min_u64(const unsigned long long* ver, int b0, int b1, long long* ds
   LSGD_CUDA(cudaGetLastError());
 }
 
+// Experimental (LSGD_B200_WAIT_MEMOP=1, A/B only): the wait as cuStreamWaitValue64 (GEQ) stream memory operations —
+// no SM slot — at the price of the device-side timeout and protocol check.
+using StreamWaitValue64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+StreamWaitValue64 stream_wait_value64() {
+  static StreamWaitValue64 fn = [] {
+    const char* e = std::getenv("LSGD_B200_WAIT_MEMOP");
+    if (!(e && std::atoi(e) != 0)) return static_cast<StreamWaitValue64>(nullptr);
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return static_cast<StreamWaitValue64>(nullptr);
+    }
+    return reinterpret_cast<StreamWaitValue64>(p);
+  }();
+  return fn;
+}
+
 void launch_wait_flags(FlagList flags, int n, unsigned long long target, unsigned long long timeout_ns,
                        volatile int* timed_out, cudaStream_t st, LaunchCounter& lc, unsigned long long max_lead) {
+  if (StreamWaitValue64 wv = max_lead != ~0ull ? stream_wait_value64() : nullptr) {
+    for (int i = 0; i < n; ++i) {
+      const CUresult r = wv(reinterpret_cast<CUstream>(st),
+                            reinterpret_cast<CUdeviceptr>(const_cast<unsigned long long*>(flags.f[i])), target,
+                            CU_STREAM_WAIT_VALUE_GEQ);
+      check<Error>(r == CUDA_SUCCESS, "cuStreamWaitValue64 failed (", static_cast<int>(r), ")");
+    }
+    return;
+  }
   wait_flags_kernel<<<1, 32, 0, st>>>(flags, n, target, max_lead, timeout_ns, timed_out);
   ++lc.n;
   LSGD_CUDA(cudaGetLastError());
