@@ -445,7 +445,7 @@ def run_b200_arm(args):
     return 0
 
 
-def self_launch(argv, n):
+def self_launch(argv, n, script=None):
     """`bench.py --gpus N` without torchrun: spawn N rank processes (one per GPU) on a 127.0.0.1 rendezvous, the
     environment torchrun would give them; rank 0's stdout is this process's stdout. Any rank failing stops the
     others and the job exits non-zero."""
@@ -458,7 +458,7 @@ def self_launch(argv, n):
     for r in range(n):
         env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
                    MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + argv, env=env,
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(script or __file__)] + argv, env=env,
                                       stdout=None if r == 0 else subprocess.DEVNULL))
     rc = 0
     try:

@@ -1,6 +1,7 @@
 """BASELINE cfg5: gradient-size sweep of the LSGD exchange (reduce, global average, broadcast, update) at 2/4/8 GPUs.
 
-    torchrun --nproc-per-node N sweep.py [--groups G] [--sizes 20,22,24,26,28,30] [--steps 20] [--warmup 5]
+    python sweep.py --gpus N [--groups G] [--sizes 20,22,24,26,28,30] [--steps 20] [--warmup 5]
+    (spawns one process per GPU like bench.py; or torchrun --nproc-per-node N sweep.py ...)
 
 Model = synthetic gradient (BASELINE cfg4/cfg5: g_r = Rng(1000 + r).next_symmetric(1.0), fp32), so a step is
 exactly the communication path: postponed update (K8) -> intra-group ordered reduce (K6) -> inter-group NCCL average
@@ -32,7 +33,12 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--global-allreduce", default="ordered", choices=["ordered", "nccl"])
+    ap.add_argument("--gpus", type=int, default=0, help="spawn this many ranks (one per GPU) when not under torchrun")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        import bench
+
+        return bench.self_launch(sys.argv[1:], args.gpus, script=__file__)
 
     import torch
     import torch.distributed as dist
@@ -111,4 +117,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())
